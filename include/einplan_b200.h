@@ -1,0 +1,112 @@
+/* einplan_b200 inner C ABI: the B200 (sm_100a) kernel layer under the
+ * einplan host API.
+ *
+ * The reference executes every binary step of a term with the host loop nest
+ * naive_evaluate (proj/src/evaluate.cpp:7-63) called per virtual rank by
+ * local_contract (proj/src/executor.cpp:126-154), then sums partial outputs
+ * with allreduce (executor.cpp:80-108) and moves intermediates with
+ * apply_plan (proj/src/redistribute.cpp:185-206).  The entry points below
+ * replace those three calls with device kernels; the host executor
+ * (einplan.h's einplan_run_json and eb_rank_*) drives them.
+ *
+ * Conventions: plain pointers and sizes only; device pointers everywhere a
+ * tensor is named; `stream` is a cudaStream_t (NULL = legacy default);
+ * return value is an eb_status (0 = ok) and eb_last_error() holds the
+ * message.  There is no CPU fallback: without a usable sm_100 device every
+ * compute entry point returns EB_E_DEVICE.
+ */
+#ifndef EINPLAN_B200_H
+#define EINPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum eb_status {
+  EB_OK = 0,
+  EB_E_INVALID = 1, /* descriptor or argument rejected */
+  EB_E_DEVICE = 2,  /* no sm_100 device / CUDA error */
+  EB_E_COMM = 3     /* collective failed */
+} eb_status;
+
+const char* eb_last_error(void);
+const char* eb_build_info(void); /* arch, nvcc version, build flags */
+
+/* One factor matrix of a Khatri-Rao row: row-major [extent][ld], columns
+ * 0..R-1 used. */
+typedef struct eb_factor {
+  const double* ptr;
+  int64_t extent;
+  int64_t ld;
+} eb_factor;
+
+enum { EB_ROW = 0, EB_COL = 1 };       /* which X dimension is contracted innermost */
+enum { EB_REDUCE = 0, EB_BATCHED = 1 }; /* sum over the outer index, or one output per outer index */
+
+/* The fused MTTKRP term / TTM step ("contraction" of one dense block).
+ *
+ * EB_ROW   X is [P][M][Q][L] row-major, contraction over l (contiguous):
+ *            out[m][r] = sum_{p,q,l} X[p,m,q,l] * KRP(pre)[p,r] * KRP(mid)[q,r] * U[l,r]
+ * EB_COL   X is [P][Q][M] row-major, contraction over q (strided):
+ *   REDUCE   out[m][r]    = sum_{p,q} X[p,q,m] * KRP(pre)[p,r] * U[q,r]
+ *   BATCHED  out[p][m][r] = sum_q     X[p,q,m] * U[q,r]          (TTM)
+ * KRP(list)[x,r] = prod_f list[f].ptr[x_f * ld_f + r], x decomposed row-major
+ * over the list's extents (empty list = 1).  U is row-major [L or Q][R].
+ * This covers order-N MTTKRP in every mode (pre = modes before the output
+ * mode, mid = modes between it and the last, U = the last (ROW) or the
+ * second-to-last (COL) mode's factor) and every TTM of the TTMc chains. */
+typedef struct eb_contract_desc {
+  int variant; /* EB_ROW / EB_COL */
+  int mode;    /* EB_REDUCE / EB_BATCHED (BATCHED requires EB_COL) */
+  int64_t P, M, Q, L; /* L ignored for EB_COL */
+  int64_t R;
+  const double* X;
+  const double* U;
+  int64_t ldu;
+  int n_pre;
+  eb_factor pre[8];
+  int n_mid;
+  eb_factor mid[8];
+  double* out;
+} eb_contract_desc;
+
+/* Device scratch the call needs (split-K partials, staged factor copies). */
+size_t eb_contract_workspace(const eb_contract_desc* d);
+int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,
+                void* stream);
+
+/* Generic binary (or unary) einsum step on dense row-major device blocks:
+ * out[...] = sum over contracted symbols of lhs[...] * rhs[...] — the GPU
+ * replacement of naive_evaluate for step shapes the fused kernels do not
+ * cover (GEMM chains, KRP, OUTER, ELEMENTWISE).  Index strings as in the
+ * reference step ("ijk,jka->ia"); `ext` gives one extent per ASCII code. */
+int eb_step_generic(const char* lhs_indices, const char* rhs_indices,
+                    const char* out_indices, const int64_t* ext, const double* lhs,
+                    const double* rhs, double* out, void* stream);
+
+/* Deterministic group sum on one device (virtual ranks): acc = 0.0, then
+ * members added in the given (ascending-rank) order; result written to
+ * every member (executor.cpp:80-108). */
+int eb_group_sum(double* const* members, int n_members, int64_t n, void* stream);
+
+/* Strided box copy of one redistribution message between dense row-major
+ * device blocks (redistribute.cpp:152-183). */
+int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst,
+                const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
+                const int64_t* ox_lo, void* stream);
+
+/* Seeded input generation identical to random_tensor (tensor.cpp:55-63):
+ * fills host memory with n values of the mt19937_64(seed) stream starting at
+ * element `skip`, using `threads` host threads (the stream is advanced by
+ * jump-free re-seeding per chunk boundary, so threads > 1 only pays off for
+ * large n). */
+void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* EINPLAN_B200_H */

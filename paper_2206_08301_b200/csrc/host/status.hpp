@@ -1,0 +1,48 @@
+// Error plumbing shared by the host layer and the kernel launchers.
+// The planner throws einplan::Error (errc carries the einplan_status); the
+// inner C ABI returns eb_status codes with a thread-local message.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "einplan_b200.h"
+
+namespace eb {
+
+void set_error(const std::string& msg);
+const char* error_cstr();
+
+// Thrown inside the launchers, mapped to eb_status at the C boundary.
+struct DeviceError : std::runtime_error {
+  explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
+};
+struct InvalidError : std::runtime_error {
+  explicit InvalidError(const std::string& m) : std::runtime_error(m) {}
+};
+
+#define EB_CUDA(call)                                                               \
+  do {                                                                              \
+    cudaError_t eb_err_ = (call);                                                   \
+    if (eb_err_ != cudaSuccess)                                                     \
+      throw ::eb::DeviceError(std::string(#call) + ": " + cudaGetErrorString(eb_err_)); \
+  } while (0)
+
+template <typename Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return EB_OK;
+  } catch (const InvalidError& e) {
+    set_error(e.what());
+    return EB_E_INVALID;
+  } catch (const DeviceError& e) {
+    set_error(e.what());
+    return EB_E_DEVICE;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return EB_E_DEVICE;
+  }
+}
+
+}  // namespace eb

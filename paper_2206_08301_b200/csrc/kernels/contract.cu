@@ -1,0 +1,648 @@
+// Fused MTTKRP term / TTM step kernel for B200 (sm_100a), FP64 on DMMA.
+//
+// Replaces, for the hot-path step shapes, the reference's per-rank loop nest
+// naive_evaluate (proj/src/evaluate.cpp:7-63) as called by local_contract
+// (proj/src/executor.cpp:126-154) for the steps of one fused term:
+//   MTTKRP  KRP steps ja,ka->jka (planner.cpp:117-119) fused with the TDOT
+//           ijk,jka->ia / ijk,ika->ja / ijk,ija->ka and, at order 5, the
+//           trailing ima,ma->ia — the Khatri-Rao rows are never stored: each
+//           KRP row is a per-(outer index, rank column) scale folded into the
+//           B fragments of the tensor-core MMA;
+//   TTM     ijk,jb->ikb and the TTMc chain steps (planner.cpp:122-127 TTM).
+//
+// Data path.  X streams from HBM exactly once through a STAGES-deep TMA ring
+// (cp.async.bulk.tensor, SWIZZLE_128B boxes of 16 doubles) filled by one
+// producer warp; NW consumer warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4,
+// the only FP64 tensor op on sm_100a — tcgen05 has no f64 kind) with
+// fragments read from the swizzled tiles bank-conflict-free: the k-order
+// inside each 16-wide box is permuted per lane (any permutation shared by the
+// A and B fragments leaves the contraction unchanged) so that the 16 lanes of
+// a half-warp hit 16 distinct bank pairs.
+//
+// Work split.  REDUCE (MTTKRP): the (row tile, outer index, k chunk) item
+// space is cut into G equal contiguous ranges, one per CTA (G = resident
+// CTAs), so every SM streams the same number of bytes; a CTA flushes its
+// register accumulators into a per-CTA partial slot whenever it leaves a row
+// tile, and eb_reduce_partials sums the slots in CTA order (deterministic:
+// no FP64 atomics, bitwise reproducible run to run like the reference's
+// ascending-rank loops).  BATCHED (TTM): one item = (row tile, outer index),
+// written straight to out[p][m][r].
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../host/status.hpp"
+#include "device_common.cuh"
+#include "einplan_b200.h"
+
+namespace eb {
+
+constexpr int kMaxFac = 8;
+
+struct FacList {
+  int n;
+  const double* ptr[kMaxFac];
+  int64_t ext[kMaxFac];
+  int64_t ld[kMaxFac];
+};
+
+struct ContractParams {
+  int64_t M;       // output rows
+  int64_t Q;       // ROW: mid extent (o = p*Q + q)
+  int64_t O;       // outer count: ROW P*Q, COL P
+  int64_t KC;      // k chunks per outer index
+  int64_t items;   // REDUCE: mtiles*O*KC ; BATCHED: mtiles*O
+  int G;           // CTAs
+  int segmax;      // partial slots per CTA (REDUCE)
+  int R;           // real columns
+  int col0;        // first rank column of this launch (R > 64 is chunked)
+  FacList pre, mid;
+  double* out;     // BATCHED: [P][M][ldo] ; REDUCE: partial slots
+  int64_t ldo;
+};
+
+__device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col) {
+  double v = 1.0;
+  for (int i = f.n - 1; i >= 0; --i) {
+    int64_t xi = x % f.ext[i];
+    x /= f.ext[i];
+    v *= __ldg(f.ptr[i] + xi * f.ld[i] + col);
+  }
+  return v;
+}
+
+template <bool COL, int MT, int NT, int KD>
+struct Tile {
+  static constexpr int kXBytes = MT * KD * 8;
+  static constexpr int kUBytes = COL ? ((NT * 8 + 15) / 16) * KD * 128 : NT * 8 * KD * 8;
+  static constexpr int kStageBytes = kXBytes + kUBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static_assert(kXBytes % 1024 == 0 && kUBytes % 1024 == 0, "swizzle atoms need 1 KB alignment");
+  static_assert(kStages >= 2, "stage too large");
+};
+
+// Store one row tile's register accumulators into this CTA's partial slot
+// `sg` and clear them.
+template <int MI, int NT, int MT, int WM>
+__device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const ContractParams& prm,
+                                              int sg, int warp, int g, int l) {
+  double* dst = prm.out + ((int64_t)blockIdx.x * prm.segmax + sg) * (int64_t)MT * (NT * 8);
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int row = warp * WM + i * 8 + g;
+      *reinterpret_cast<double2*>(dst + row * (NT * 8) + j * 8 + 2 * l) =
+          make_double2(acc[i][j][0], acc[i][j][1]);
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+}
+
+template <bool COL, bool BATCHED, int NW, int WM, int NT, int KD>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    contract_kernel(const __grid_constant__ CUtensorMap xmap,
+                    const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
+  constexpr int MT = NW * WM;
+  constexpr int MI = WM / 8;  // m8 tiles per warp
+  using T = Tile<COL, MT, NT, KD>;
+  constexpr int S = T::kStages;
+
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_addr(&full_bar[s]), 1);
+      mbar_init(smem_addr(&empty_bar[s]), NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // Item range of this CTA.
+  const int64_t i0 = (int64_t)blockIdx.x * prm.items / prm.G;
+  const int64_t i1 = (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
+  const int64_t per_tile = BATCHED ? prm.O : prm.O * prm.KC;
+
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch_desc(&xmap);
+      tma_prefetch_desc(&umap);
+      uint32_t it = 0;
+      for (int64_t item = i0; item < i1; ++item) {
+        const int64_t mt = item / per_tile;
+        const int64_t o = BATCHED ? item % prm.O : (item / prm.KC) % prm.O;
+        const int64_t kc_begin = BATCHED ? 0 : item % prm.KC;
+        const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
+        for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
+          const int st = it % S;
+          if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
+          const uint32_t fb = smem_addr(&full_bar[st]);
+          mbar_expect_tx(fb, T::kStageBytes);
+          const uint32_t xs = base + st * T::kStageBytes;
+          const uint32_t us = xs + T::kXBytes;
+          const int k0 = (int)(kc * KD);
+          if (!COL) {
+            const int p = (int)(o / prm.Q), q = (int)(o % prm.Q);
+#pragma unroll
+            for (int b = 0; b < KD / 16; ++b) {
+              tma_load_4d(xs + b * MT * 128, &xmap, fb, k0 + 16 * b, q, (int)(mt * MT), p);
+              tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, 0);
+            }
+          } else {
+#pragma unroll
+            for (int b = 0; b < MT / 16; ++b)
+              tma_load_3d(xs + b * KD * 128, &xmap, fb, (int)(mt * MT) + 16 * b, k0, (int)o);
+#pragma unroll
+            for (int b = 0; b < (NT * 8 + 15) / 16; ++b)
+              tma_load_2d(us + b * KD * 128, &umap, fb, prm.col0 + 16 * b, k0);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int g = lane >> 2, l = lane & 3;
+  double acc[MI][NT][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Per-lane byte offsets inside a 128-B swizzled row for the 4 k-steps of
+  // a 16-wide box (see the header comment for the bank argument).
+  //   ROW: lane reads k = 2s + (l&1) + 8(l>>1) of row (..8i+g)
+  //   COL: lane reads row k = 2l + (s&1) + 8(s>>1), column (..8i+g)
+  uint32_t off_a[4][2], off_b[4][2];  // [s][odd m8/n8 tile within a 16-box]
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!COL) {
+        const uint32_t chunk = (uint32_t)((s + 4 * (l >> 1)) ^ g);
+        off_a[s][h] = g * 128 + chunk * 16 + (l & 1) * 8;
+        off_b[s][h] = off_a[s][h];
+      } else {
+        const int krow = 2 * l + (s & 1) + 8 * (s >> 1);
+        const uint32_t chunk = (uint32_t)((4 * h + (g >> 1)) ^ (krow & 7));
+        off_a[s][h] = krow * 128 + chunk * 16 + (g & 1) * 8;
+        off_b[s][h] = off_a[s][h];
+      }
+    }
+  }
+
+  double scale[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) scale[j] = 1.0;
+
+  int64_t cur_mt = -1, cur_o = -1;
+  int seg = -1;
+  uint32_t it = 0;
+
+  for (int64_t item = i0; item < i1; ++item) {
+    const int64_t mt = item / per_tile;
+    const int64_t o = BATCHED ? item % prm.O : (item / prm.KC) % prm.O;
+    const int64_t kc_begin = BATCHED ? 0 : item % prm.KC;
+    const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
+    if (!BATCHED) {
+      if (mt != cur_mt) {
+        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM>(acc, prm, seg, warp, g, l);
+        ++seg;
+        cur_mt = mt;
+      }
+      if (o != cur_o) {
+        cur_o = o;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int col = j * 8 + g;
+          double v = 0.0;
+          if (prm.col0 + col < prm.R && col < NT * 8) {
+            const int gc = prm.col0 + col;
+            if (!COL) {
+              v = krp_value(prm.pre, o / prm.Q, gc) * krp_value(prm.mid, o % prm.Q, gc);
+            } else {
+              v = krp_value(prm.pre, o, gc);
+            }
+          }
+          scale[j] = v;
+        }
+      }
+    }
+    for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
+      const int st = it % S;
+      mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
+      const uint8_t* xs = sbase + st * T::kStageBytes;
+      const uint8_t* us = xs + T::kXBytes;
+#pragma unroll
+      for (int b16 = 0; b16 < KD / 16; ++b16) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double a[MI], bf[NT];
+#pragma unroll
+          for (int i = 0; i < MI; ++i) {
+            const int m8 = warp * MI + i;  // m8 tile index inside the CTA tile
+            uint32_t off;
+            if (!COL)
+              off = b16 * MT * 128 + m8 * 8 * 128 + off_a[s][0];
+            else
+              off = (m8 >> 1) * KD * 128 + b16 * 16 * 128 + off_a[s][m8 & 1];
+            a[i] = *reinterpret_cast<const double*>(xs + off);
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            uint32_t off;
+            if (!COL)
+              off = b16 * NT * 8 * 128 + j * 8 * 128 + off_b[s][0];
+            else
+              off = (j >> 1) * KD * 128 + b16 * 16 * 128 + off_b[s][j & 1];
+            const double u = *reinterpret_cast<const double*>(us + off);
+            bf[j] = BATCHED ? u : u * scale[j];
+          }
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
+    }
+    if (BATCHED) {
+      // out[p][m][col0 + n], guarded at the ragged row / column edges.
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int64_t row = mt * MT + warp * WM + i * 8 + g;
+        if (row < prm.M) {
+          double* dst = prm.out + (o * prm.M + row) * prm.ldo + prm.col0;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int c = j * 8 + 2 * l;
+            const int gc = prm.col0 + c;
+            if (gc + 1 < prm.R && ((reinterpret_cast<uintptr_t>(dst + c) & 15) == 0)) {
+              *reinterpret_cast<double2*>(dst + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+            } else {
+              if (gc < prm.R) dst[c] = acc[i][j][0];
+              if (gc + 1 < prm.R) dst[c + 1] = acc[i][j][1];
+            }
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+      }
+    }
+  }
+  if (!BATCHED && cur_mt >= 0) flush_partial<MI, NT, MT, WM>(acc, prm, seg, warp, g, l);
+}
+
+// Deterministic split-K finish: out[m][col0+n] = sum over CTAs (ascending)
+// of their partial slot for tile m / MT.
+__global__ void reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out,
+                                       int64_t M, int R, int col0, int64_t ldo, int NP, int MT,
+                                       int64_t per_tile, int64_t items, int G, int segmax) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * NP) return;
+  const int64_t m = idx / NP;
+  const int n = (int)(idx % NP);
+  if (col0 + n >= R) return;
+  const int64_t t = m / MT;
+  const int64_t lo = t * per_tile, hi = lo + per_tile;
+  double acc = 0.0;
+  for (int c = 0; c < G; ++c) {
+    const int64_t c0 = (int64_t)c * items / G, c1 = (int64_t)(c + 1) * items / G;
+    if (c1 <= lo || c0 >= hi || c1 <= c0) continue;
+    const int64_t sg = t - c0 / per_tile;
+    acc += ws[(((int64_t)c * segmax + sg) * MT + (m % MT)) * NP + n];
+  }
+  out[m * ldo + col0 + n] = acc;
+}
+
+// Uᵀ staging for the ROW variant (TMA needs k innermost): ut[n][l] = u[l][col0+n].
+__global__ void transpose_factor_kernel(const double* __restrict__ u, int64_t ldu, int64_t L,
+                                        int cols, int col0, double* __restrict__ ut, int64_t ldt) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)cols * L) return;
+  const int n = (int)(idx / L);
+  const int64_t k = idx % L;
+  ut[n * ldt + k] = u[k * ldu + col0 + n];
+}
+
+// COL staging: copy into an even-pitched [Q][pitch] buffer (TMA strides are
+// multiples of 16 B).
+__global__ void pitch_factor_kernel(const double* __restrict__ u, int64_t ldu, int64_t Q, int R,
+                                    double* __restrict__ up, int64_t pitch) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Q * pitch) return;
+  const int64_t q = idx / pitch;
+  const int n = (int)(idx % pitch);
+  up[idx] = n < R ? u[q * ldu + n] : 0.0;
+}
+
+// ------------------------------------------------------------------ host --
+
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) throw DeviceError("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+CUtensorMap make_map(const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                     const uint32_t* box) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) s[i] = strides_bytes[i];
+  }
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(ptr), d, s,
+                         b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw InvalidError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EB_CUDA(cudaGetDevice(&dev));
+    EB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+void check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw DeviceError("no CUDA device");
+  int major = 0;
+  EB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw DeviceError("einplan_b200 kernels are built for sm_100a only");
+}
+
+FacList to_list(int n, const eb_factor* f) {
+  FacList l;
+  std::memset(&l, 0, sizeof(l));
+  if (n < 0 || n > kMaxFac) throw InvalidError("eb_contract: at most 8 factors per KRP list");
+  l.n = n;
+  for (int i = 0; i < n; ++i) {
+    if (!f[i].ptr || f[i].extent < 1) throw InvalidError("eb_contract: bad factor");
+    l.ptr[i] = f[i].ptr;
+    l.ext[i] = f[i].extent;
+    l.ld[i] = f[i].ld;
+  }
+  return l;
+}
+
+struct Plan {
+  bool col = false, batched = false;
+  int nw = 4, wm = 32, nt = 4, kd = 32;
+  int mt = 128;
+  int64_t kin = 0, O = 0, KC = 0, mtiles = 0, items = 0;
+  int G = 0, segmax = 0;
+  int chunks = 1;      // rank-column chunks of <= 64
+  size_t u_bytes = 0;  // staged factor buffer (per chunk)
+  size_t ws_bytes = 0; // partial slots (per chunk)
+};
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+Plan plan_of(const eb_contract_desc* d) {
+  if (!d) throw InvalidError("eb_contract: null descriptor");
+  if (d->variant != EB_ROW && d->variant != EB_COL) throw InvalidError("eb_contract: bad variant");
+  if (d->mode != EB_REDUCE && d->mode != EB_BATCHED) throw InvalidError("eb_contract: bad mode");
+  if (d->mode == EB_BATCHED && d->variant != EB_COL)
+    throw InvalidError("eb_contract: BATCHED requires the COL variant");
+  if (d->P < 1 || d->M < 1 || d->Q < 1 || d->R < 1 || (d->variant == EB_ROW && d->L < 1))
+    throw InvalidError("eb_contract: extents must be positive");
+  if (!d->X || !d->U || !d->out) throw InvalidError("eb_contract: null tensor");
+  Plan p;
+  p.col = d->variant == EB_COL;
+  p.batched = d->mode == EB_BATCHED;
+  // TMA: row pitch of X must be a multiple of 16 bytes.
+  if ((p.col ? d->M : d->L) % 2 != 0)
+    throw InvalidError("eb_contract: innermost X extent must be even (TMA 16-B pitch)");
+  const int64_t rcols = std::min<int64_t>(d->R, 64);
+  p.chunks = (int)cdiv(d->R, 64);
+  p.nt = (int)cdiv(rcols, 8);
+  const int64_t rows = d->M;
+  p.wm = rows >= 128 && (p.batched || p.nt <= 4) ? 32 : 16;
+  p.mt = p.nw * p.wm;
+  p.kd = 32;
+  p.kin = p.col ? d->Q : d->L;
+  p.O = p.col ? d->P : d->P * d->Q;
+  p.KC = cdiv(p.kin, p.kd);
+  p.mtiles = cdiv(rows, p.mt);
+  const int sms = sm_count();
+  if (p.batched) {
+    p.items = p.mtiles * p.O;
+    p.G = (int)std::min<int64_t>(p.items, (int64_t)sms);
+  } else {
+    p.items = p.mtiles * p.O * p.KC;
+    p.G = (int)std::min<int64_t>(p.items, (int64_t)sms);
+    const int64_t per_tile = p.O * p.KC;
+    int segmax = 1;
+    for (int c = 0; c < p.G; ++c) {
+      const int64_t c0 = (int64_t)c * p.items / p.G, c1 = (int64_t)(c + 1) * p.items / p.G;
+      if (c1 > c0) segmax = std::max<int>(segmax, (int)((c1 - 1) / per_tile - c0 / per_tile + 1));
+    }
+    p.segmax = segmax;
+    p.ws_bytes = (size_t)p.G * segmax * p.mt * (p.nt * 8) * sizeof(double);
+  }
+  if (p.col) {
+    p.u_bytes = (size_t)d->Q * ((d->R + 1) / 2 * 2) * sizeof(double);
+  } else {
+    p.u_bytes = (size_t)p.nt * 8 * ((d->L + 1) / 2 * 2) * sizeof(double);
+  }
+  p.u_bytes = (p.u_bytes + 255) / 256 * 256;
+  p.ws_bytes = (p.ws_bytes + 255) / 256 * 256;
+  return p;
+}
+
+template <bool COL, bool BATCHED, int NW, int WM, int NT, int KD>
+void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
+              cudaStream_t st) {
+  using T = Tile<COL, NW * WM, NT, KD>;
+  auto kern = contract_kernel<COL, BATCHED, NW, WM, NT, KD>;
+  static bool attr = false;
+  if (!attr) {
+    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
+    attr = true;
+  }
+  kern<<<prm.G, (NW + 1) * 32, T::kSmem, st>>>(xm, um, prm);
+  EB_CUDA(cudaGetLastError());
+}
+
+template <bool COL, bool BATCHED, int WM>
+void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
+                 cudaStream_t st) {
+  switch (nt) {
+    case 1: return launch_t<COL, BATCHED, 4, WM, 1, 32>(xm, um, prm, st);
+    case 2: return launch_t<COL, BATCHED, 4, WM, 2, 32>(xm, um, prm, st);
+    case 3: return launch_t<COL, BATCHED, 4, WM, 3, 32>(xm, um, prm, st);
+    case 4: return launch_t<COL, BATCHED, 4, WM, 4, 32>(xm, um, prm, st);
+    case 5: return launch_t<COL, BATCHED, 4, WM, 5, 32>(xm, um, prm, st);
+    case 6: return launch_t<COL, BATCHED, 4, WM, 6, 32>(xm, um, prm, st);
+    case 7: return launch_t<COL, BATCHED, 4, WM, 7, 32>(xm, um, prm, st);
+    case 8: return launch_t<COL, BATCHED, 4, WM, 8, 32>(xm, um, prm, st);
+  }
+  throw InvalidError("eb_contract: unsupported column tile count");
+}
+
+void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
+                    const ContractParams& prm, cudaStream_t st) {
+  if (p.col && p.batched) {
+    if (p.wm == 32) dispatch_nt<true, true, 32>(nt, xm, um, prm, st);
+    else dispatch_nt<true, true, 16>(nt, xm, um, prm, st);
+  } else if (p.col) {
+    if (p.wm == 32) dispatch_nt<true, false, 32>(nt, xm, um, prm, st);
+    else dispatch_nt<true, false, 16>(nt, xm, um, prm, st);
+  } else {
+    if (p.wm == 32) dispatch_nt<false, false, 32>(nt, xm, um, prm, st);
+    else dispatch_nt<false, false, 16>(nt, xm, um, prm, st);
+  }
+}
+
+void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStream_t st) {
+  check_device();
+  const Plan p = plan_of(d);
+  const size_t need = (p.u_bytes + p.ws_bytes);
+  if (ws_bytes < need) throw InvalidError("eb_contract: workspace too small");
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  double* ubuf = reinterpret_cast<double*>(wsb);
+  double* part = reinterpret_cast<double*>(wsb + p.u_bytes);
+
+  ContractParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.M = d->M;
+  prm.Q = d->Q;
+  prm.O = p.O;
+  prm.KC = p.KC;
+  prm.items = p.items;
+  prm.G = p.G;
+  prm.segmax = p.segmax;
+  prm.R = (int)d->R;
+  prm.pre = to_list(d->n_pre, d->pre);
+  prm.mid = to_list(p.col ? 0 : d->n_mid, d->mid);
+  const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
+
+  // COL stages the whole factor once (pitch = even R); ROW stages Uᵀ per
+  // 64-column chunk.
+  int64_t pitch = (d->R + 1) / 2 * 2;
+  CUtensorMap umap_col;
+  if (p.col) {
+    const int64_t n = d->Q * pitch;
+    pitch_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->Q, (int)d->R, ubuf,
+                                                                 pitch);
+    EB_CUDA(cudaGetLastError());
+    const uint64_t dims[2] = {(uint64_t)d->R, (uint64_t)d->Q};
+    const uint64_t str[1] = {(uint64_t)pitch * 8};
+    const uint32_t box[2] = {16, (uint32_t)p.kd};
+    umap_col = make_map(ubuf, 2, dims, str, box);
+  }
+  CUtensorMap xmap;
+  if (!p.col) {
+    const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->Q, (uint64_t)d->M, (uint64_t)d->P};
+    const uint64_t str[3] = {(uint64_t)d->L * 8, (uint64_t)(d->Q * d->L) * 8,
+                             (uint64_t)(d->M * d->Q * d->L) * 8};
+    const uint32_t box[4] = {16, 1, (uint32_t)p.mt, 1};
+    xmap = make_map(d->X, 4, dims, str, box);
+  } else {
+    const uint64_t dims[3] = {(uint64_t)d->M, (uint64_t)d->Q, (uint64_t)d->P};
+    const uint64_t str[2] = {(uint64_t)d->M * 8, (uint64_t)(d->Q * d->M) * 8};
+    const uint32_t box[3] = {16, (uint32_t)p.kd, 1};
+    xmap = make_map(d->X, 3, dims, str, box);
+  }
+
+  for (int c = 0; c < p.chunks; ++c) {
+    const int col0 = c * 64;
+    const int cols = (int)std::min<int64_t>(64, d->R - col0);
+    const int nt = (int)cdiv(cols, 8);
+    prm.col0 = col0;
+    CUtensorMap umap;
+    if (!p.col) {
+      const int64_t lp = (d->L + 1) / 2 * 2;
+      const int64_t n = (int64_t)cols * d->L;
+      transpose_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->L, cols, col0,
+                                                                       ubuf, lp);
+      EB_CUDA(cudaGetLastError());
+      const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)cols};
+      const uint64_t str[1] = {(uint64_t)lp * 8};
+      const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
+      umap = make_map(ubuf, 2, dims, str, box);
+    } else {
+      umap = umap_col;
+    }
+    ContractParams q = prm;
+    q.out = p.batched ? d->out : part;
+    q.ldo = d->R;
+    launch_variant(p, nt, xmap, umap, q, st);
+    if (!p.batched) {
+      const int np = nt * 8;
+      const int64_t n = d->M * np;
+      reduce_partials_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(
+          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.O * p.KC, p.items, p.G,
+          p.segmax);
+      EB_CUDA(cudaGetLastError());
+    }
+  }
+}
+
+}  // namespace
+
+}  // namespace eb
+
+extern "C" size_t eb_contract_workspace(const eb_contract_desc* d) {
+  try {
+    eb::Plan p = eb::plan_of(d);
+    return p.u_bytes + p.ws_bytes;
+  } catch (const std::exception& e) {
+    eb::set_error(e.what());
+    return 0;
+  }
+}
+
+extern "C" int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  return eb::guard([&] {
+    eb::run_contract(d, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
