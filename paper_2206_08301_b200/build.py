@@ -34,6 +34,17 @@ def _nccl_root():
     return None
 
 
+def _nlohmann():
+    """nlohmann/json 3.11.3 as shipped inside cudnn_frontend in this image (the
+    same library the reference uses for its einplan/v1 reports)."""
+    import sysconfig
+    base = os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend",
+                        "thirdparty")
+    if not os.path.exists(os.path.join(base, "nlohmann", "json.hpp")):
+        raise RuntimeError("nlohmann/json.hpp not found under " + base)
+    return base
+
+
 def _headers():
     hs = glob.glob(os.path.join(CSRC, "**", "*.h*"), recursive=True)
     hs += glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True)
@@ -46,7 +57,7 @@ def _compile(src: str, hdr_time: float, nccl: str | None) -> str:
     obj = os.path.join(OBJ, rel + ".o")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_time):
         return obj
-    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-isystem", _nlohmann()]
     defs = []
     if nccl:
         inc.append("-I" + os.path.join(nccl, "include"))

@@ -76,42 +76,79 @@ __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col
   return v;
 }
 
+// Shared-memory stage: X tile, U tile, and (REDUCE) the stage's Khatri-Rao
+// scale row.  Every piece starts on a 1 KB boundary (SWIZZLE_128B atoms).
 template <bool COL, int MT, int NT, int KD>
 struct Tile {
   static constexpr int kXBytes = MT * KD * 8;
   static constexpr int kUBytes = COL ? ((NT * 8 + 15) / 16) * KD * 128 : NT * 8 * KD * 8;
-  static constexpr int kStageBytes = kXBytes + kUBytes;
+  static constexpr int kScaleBytes = 1024;  // NT*8 <= 64 doubles
+  static constexpr int kStageBytes = kXBytes + kUBytes + kScaleBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static_assert(kXBytes % 1024 == 0 && kUBytes % 1024 == 0, "swizzle atoms need 1 KB alignment");
   static_assert(kStages >= 2, "stage too large");
 };
 
-// Store one row tile's register accumulators into this CTA's partial slot
-// `sg` and clear them.
-template <int MI, int NT, int MT, int WM>
+// Position in the (row tile, outer index, k chunk) item space, advanced
+// incrementally (no 64-bit division on the per-stage path).
+struct Cursor {
+  int64_t mt, o, kc;
+  __device__ __forceinline__ void seek(int64_t item, bool batched, const ContractParams& p) {
+    if (batched) {
+      kc = 0;
+      o = item % p.O;
+      mt = item / p.O;
+    } else {
+      kc = item % p.KC;
+      const int64_t t = item / p.KC;
+      o = t % p.O;
+      mt = t / p.O;
+    }
+  }
+  __device__ __forceinline__ void advance(bool batched, const ContractParams& p) {
+    if (!batched && ++kc < p.KC) return;
+    kc = 0;
+    if (++o < p.O) return;
+    o = 0;
+    ++mt;
+  }
+};
+
+// Store one row tile's register accumulators into partial slot (sg, ks) of
+// this CTA and clear them.
+template <int MI, int NT, int MT, int WM, int KS>
 __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const ContractParams& prm,
-                                              int sg, int warp, int g, int l) {
-  double* dst = prm.out + ((int64_t)blockIdx.x * prm.segmax + sg) * (int64_t)MT * (NT * 8);
+                                              int sg, int wm, int ks, int g, int l) {
+  double* dst = prm.out +
+                (((int64_t)blockIdx.x * prm.segmax + sg) * KS + ks) * (int64_t)MT * (NT * 8);
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
-      const int row = warp * WM + i * 8 + g;
+      const int row = wm * WM + i * 8 + g;
       *reinterpret_cast<double2*>(dst + row * (NT * 8) + j * 8 + 2 * l) =
           make_double2(acc[i][j][0], acc[i][j][1]);
       acc[i][j][0] = acc[i][j][1] = 0.0;
     }
 }
 
-template <bool COL, bool BATCHED, int NW, int WM, int NT, int KD>
-__global__ void __launch_bounds__((NW + 1) * 32, 1)
+// Warp roles: warp NWM*KS is the producer (all 32 lanes compute the stage's
+// Khatri-Rao scale row, lane 0 issues the TMA boxes); consumer warp w owns
+// rows (w % NWM)*WM.. of the CTA tile and the 16-deep k groups g16 of each
+// stage with g16 % KS == w / NWM (k split inside the CTA; REDUCE keeps one
+// partial per k-split group, BATCHED requires KS == 1).
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT>
+__global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
-  constexpr int MT = NW * WM;
+  static_assert(KD % (16 * KS) == 0, "each k-split group owns whole 16-deep groups");
+  constexpr int MT = NWM * WM;
   constexpr int MI = WM / 8;  // m8 tiles per warp
+  constexpr int NCW = NWM * KS;
   using T = Tile<COL, MT, NT, KD>;
   constexpr int S = T::kStages;
+  static_assert(!BATCHED || KS == 1, "BATCHED writes each unit once");
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
@@ -127,33 +164,56 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_addr(&full_bar[s]), 1);
-      mbar_init(smem_addr(&empty_bar[s]), NW);
+      mbar_init(smem_addr(&empty_bar[s]), NCW);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  // Item range of this CTA.
   const int64_t i0 = (int64_t)blockIdx.x * prm.items / prm.G;
   const int64_t i1 = (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
-  const int64_t per_tile = BATCHED ? prm.O : prm.O * prm.KC;
 
-  if (warp == NW) {
+  if (warp == NCW) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       tma_prefetch_desc(&xmap);
       tma_prefetch_desc(&umap);
-      uint32_t it = 0;
-      for (int64_t item = i0; item < i1; ++item) {
-        const int64_t mt = item / per_tile;
-        const int64_t o = BATCHED ? item % prm.O : (item / prm.KC) % prm.O;
-        const int64_t kc_begin = BATCHED ? 0 : item % prm.KC;
-        const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
-        for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
-          const int st = it % S;
-          if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
+    }
+    uint32_t it = 0;
+    int64_t scale_o = -1;
+    double sc0 = 0.0, sc1 = 0.0;  // scale for columns lane, lane + 32
+    Cursor cur;
+    cur.seek(i0, BATCHED, prm);
+    for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
+      const int64_t mt = cur.mt, o = cur.o;
+      const int64_t kc_begin = cur.kc;
+      const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
+      if (!BATCHED && o != scale_o) {
+        scale_o = o;
+        const int64_t p = COL ? o : o / prm.Q;
+        for (int h = 0; h < 2; ++h) {
+          const int col = lane + 32 * h;
+          double v = 0.0;
+          if (col < NT * 8 && prm.col0 + col < prm.R) {
+            v = krp_value(prm.pre, p, prm.col0 + col);
+            if (!COL) v *= krp_value(prm.mid, o % prm.Q, prm.col0 + col);
+          }
+          (h ? sc1 : sc0) = v;
+        }
+      }
+      for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
+        const int st = it % S;
+        if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
+        uint8_t* stage = sbase + st * T::kStageBytes;
+        if (!BATCHED) {
+          double* sc = reinterpret_cast<double*>(stage + T::kXBytes + T::kUBytes);
+          if (lane < NT * 8) sc[lane] = sc0;
+          if (lane + 32 < NT * 8) sc[lane + 32] = sc1;
+        }
+        __syncwarp();
+        if (lane == 0) {
           const uint32_t fb = smem_addr(&full_bar[st]);
-          mbar_expect_tx(fb, T::kStageBytes);
+          mbar_expect_tx(fb, T::kXBytes + T::kUBytes);
           const uint32_t xs = base + st * T::kStageBytes;
           const uint32_t us = xs + T::kXBytes;
           const int k0 = (int)(kc * KD);
@@ -179,6 +239,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   }
 
   // -------------------------------------------------------------- consumers
+  const int wm = warp % NWM, ks = warp / NWM;
   const int g = lane >> 2, l = lane & 3;
   double acc[MI][NT][2];
 #pragma unroll
@@ -187,99 +248,80 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   // Per-lane byte offsets inside a 128-B swizzled row for the 4 k-steps of
-  // a 16-wide box (see the header comment for the bank argument).
+  // a 16-deep group (see the header comment for the bank argument).
   //   ROW: lane reads k = 2s + (l&1) + 8(l>>1) of row (..8i+g)
   //   COL: lane reads row k = 2l + (s&1) + 8(s>>1), column (..8i+g)
-  uint32_t off_a[4][2], off_b[4][2];  // [s][odd m8/n8 tile within a 16-box]
+  uint32_t off[4][2];  // [s][odd m8/n8 tile within a 16-wide box]
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!COL) {
         const uint32_t chunk = (uint32_t)((s + 4 * (l >> 1)) ^ g);
-        off_a[s][h] = g * 128 + chunk * 16 + (l & 1) * 8;
-        off_b[s][h] = off_a[s][h];
+        off[s][h] = g * 128 + chunk * 16 + (l & 1) * 8;
       } else {
         const int krow = 2 * l + (s & 1) + 8 * (s >> 1);
         const uint32_t chunk = (uint32_t)((4 * h + (g >> 1)) ^ (krow & 7));
-        off_a[s][h] = krow * 128 + chunk * 16 + (g & 1) * 8;
-        off_b[s][h] = off_a[s][h];
+        off[s][h] = krow * 128 + chunk * 16 + (g & 1) * 8;
       }
     }
   }
 
-  double scale[NT];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) scale[j] = 1.0;
-
-  int64_t cur_mt = -1, cur_o = -1;
+  int64_t cur_mt = -1;
   int seg = -1;
   uint32_t it = 0;
 
-  for (int64_t item = i0; item < i1; ++item) {
-    const int64_t mt = item / per_tile;
-    const int64_t o = BATCHED ? item % prm.O : (item / prm.KC) % prm.O;
-    const int64_t kc_begin = BATCHED ? 0 : item % prm.KC;
+  Cursor cur;
+  cur.seek(i0, BATCHED, prm);
+  for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
+    const int64_t mt = cur.mt, o = cur.o;
+    const int64_t kc_begin = cur.kc;
     const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
-    if (!BATCHED) {
-      if (mt != cur_mt) {
-        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM>(acc, prm, seg, warp, g, l);
-        ++seg;
-        cur_mt = mt;
-      }
-      if (o != cur_o) {
-        cur_o = o;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          const int col = j * 8 + g;
-          double v = 0.0;
-          if (prm.col0 + col < prm.R && col < NT * 8) {
-            const int gc = prm.col0 + col;
-            if (!COL) {
-              v = krp_value(prm.pre, o / prm.Q, gc) * krp_value(prm.mid, o % prm.Q, gc);
-            } else {
-              v = krp_value(prm.pre, o, gc);
-            }
-          }
-          scale[j] = v;
-        }
-      }
+    if (!BATCHED && mt != cur_mt) {
+      if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(acc, prm, seg, wm, ks, g, l);
+      ++seg;
+      cur_mt = mt;
     }
     for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
       const int st = it % S;
       mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
       const uint8_t* xs = sbase + st * T::kStageBytes;
       const uint8_t* us = xs + T::kXBytes;
+      double scale[NT];
+      if (!BATCHED) {
+        const double* sc = reinterpret_cast<const double*>(us + T::kUBytes);
 #pragma unroll
-      for (int b16 = 0; b16 < KD / 16; ++b16) {
+        for (int j = 0; j < NT; ++j) scale[j] = sc[j * 8 + g];
+      }
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          double a[MI], bf[NT];
+      for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
 #pragma unroll
-          for (int i = 0; i < MI; ++i) {
-            const int m8 = warp * MI + i;  // m8 tile index inside the CTA tile
-            uint32_t off;
-            if (!COL)
-              off = b16 * MT * 128 + m8 * 8 * 128 + off_a[s][0];
-            else
-              off = (m8 >> 1) * KD * 128 + b16 * 16 * 128 + off_a[s][m8 & 1];
-            a[i] = *reinterpret_cast<const double*>(xs + off);
-          }
+      for (int s = 0; s < 4; ++s) {
+        double a[MI], bf[NT];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            uint32_t off;
-            if (!COL)
-              off = b16 * NT * 8 * 128 + j * 8 * 128 + off_b[s][0];
-            else
-              off = (j >> 1) * KD * 128 + b16 * 16 * 128 + off_b[s][j & 1];
-            const double u = *reinterpret_cast<const double*>(us + off);
-            bf[j] = BATCHED ? u : u * scale[j];
-          }
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
+        for (int i = 0; i < MI; ++i) {
+          const int m8 = wm * MI + i;  // m8 tile index inside the CTA tile
+          uint32_t o_a;
+          if (!COL)
+            o_a = b16 * MT * 128 + m8 * 8 * 128 + off[s][0];
+          else
+            o_a = (m8 >> 1) * KD * 128 + b16 * 16 * 128 + off[s][m8 & 1];
+          a[i] = *reinterpret_cast<const double*>(xs + o_a);
         }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          uint32_t o_b;
+          if (!COL)
+            o_b = b16 * NT * 8 * 128 + j * 8 * 128 + off[s][0];
+          else
+            o_b = (j >> 1) * KD * 128 + b16 * 16 * 128 + off[s][j & 1];
+          const double u = *reinterpret_cast<const double*>(us + o_b);
+          bf[j] = BATCHED ? u : u * scale[j];
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bf[j]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
@@ -288,7 +330,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       // out[p][m][col0 + n], guarded at the ragged row / column edges.
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
-        const int64_t row = mt * MT + warp * WM + i * 8 + g;
+        const int64_t row = mt * MT + wm * WM + i * 8 + g;
         if (row < prm.M) {
           double* dst = prm.out + (o * prm.M + row) * prm.ldo + prm.col0;
 #pragma unroll
@@ -310,14 +352,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       }
     }
   }
-  if (!BATCHED && cur_mt >= 0) flush_partial<MI, NT, MT, WM>(acc, prm, seg, warp, g, l);
+  if (!BATCHED && cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(acc, prm, seg, wm, ks, g, l);
 }
 
-// Deterministic split-K finish: out[m][col0+n] = sum over CTAs (ascending)
-// of their partial slot for tile m / MT.
+// Deterministic split-K finish: out[m][col0+n] = sum over CTAs (ascending),
+// then over the CTA's k-split groups, of their partial slot for tile m / MT.
 __global__ void reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out,
                                        int64_t M, int R, int col0, int64_t ldo, int NP, int MT,
-                                       int64_t per_tile, int64_t items, int G, int segmax) {
+                                       int KS, int64_t per_tile, int64_t items, int G,
+                                       int segmax) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= M * NP) return;
   const int64_t m = idx / NP;
@@ -325,12 +368,17 @@ __global__ void reduce_partials_kernel(const double* __restrict__ ws, double* __
   if (col0 + n >= R) return;
   const int64_t t = m / MT;
   const int64_t lo = t * per_tile, hi = lo + per_tile;
+  // CTAs c with [c*items/G, (c+1)*items/G) overlapping [lo, hi):
+  //   c >= ceil((lo+1)*G/items) - 1  and  c <= ceil(hi*G/items) - 1.
+  const int64_t cmin = ((lo + 1) * G + items - 1) / items - 1;
+  const int64_t cmax = (hi * G + items - 1) / items - 1;
   double acc = 0.0;
-  for (int c = 0; c < G; ++c) {
-    const int64_t c0 = (int64_t)c * items / G, c1 = (int64_t)(c + 1) * items / G;
+  for (int64_t c = cmin < 0 ? 0 : cmin; c <= cmax && c < G; ++c) {
+    const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
     if (c1 <= lo || c0 >= hi || c1 <= c0) continue;
     const int64_t sg = t - c0 / per_tile;
-    acc += ws[(((int64_t)c * segmax + sg) * MT + (m % MT)) * NP + n];
+    for (int k = 0; k < KS; ++k)
+      acc += ws[(((c * segmax + sg) * KS + k) * MT + (m % MT)) * NP + n];
   }
   out[m * ldo + col0 + n] = acc;
 }
@@ -434,7 +482,7 @@ FacList to_list(int n, const eb_factor* f) {
 
 struct Plan {
   bool col = false, batched = false;
-  int nw = 4, wm = 32, nt = 4, kd = 32;
+  int nwm = 4, wm = 32, ks = 2, kd = 32, nt = 4;
   int mt = 128;
   int64_t kin = 0, O = 0, KC = 0, mtiles = 0, items = 0;
   int G = 0, segmax = 0;
@@ -464,9 +512,22 @@ Plan plan_of(const eb_contract_desc* d) {
   p.chunks = (int)cdiv(d->R, 64);
   p.nt = (int)cdiv(rcols, 8);
   const int64_t rows = d->M;
-  p.wm = rows >= 128 && (p.batched || p.nt <= 4) ? 32 : 16;
-  p.mt = p.nw * p.wm;
-  p.kd = 32;
+  // Tile configurations (instantiated in dispatch below):
+  //   REDUCE, M >= 128 : 4 row warps x 32 rows, k split 2, 32-deep stages
+  //   REDUCE, M <  128 : 2 row warps x 32 rows, k split 4, 64-deep stages
+  //   REDUCE, R >  32  : 4 row warps x 16 rows, k split 2 (register budget:
+  //                      9 warps leave 168 registers per thread)
+  //   BATCHED          : 4 row warps x 32 (M >= 128) or 16 rows, 32-deep
+  if (p.batched) {
+    p.nwm = 4; p.wm = rows >= 128 ? 32 : 16; p.ks = 1; p.kd = 32;
+  } else if (p.nt > 4) {
+    p.nwm = 4; p.wm = 16; p.ks = 2; p.kd = 32;
+  } else if (rows >= 128) {
+    p.nwm = 4; p.wm = 32; p.ks = 2; p.kd = 32;
+  } else {
+    p.nwm = 2; p.wm = 32; p.ks = 4; p.kd = 64;
+  }
+  p.mt = p.nwm * p.wm;
   p.kin = p.col ? d->Q : d->L;
   p.O = p.col ? d->P : d->P * d->Q;
   p.KC = cdiv(p.kin, p.kd);
@@ -485,7 +546,7 @@ Plan plan_of(const eb_contract_desc* d) {
       if (c1 > c0) segmax = std::max<int>(segmax, (int)((c1 - 1) / per_tile - c0 / per_tile + 1));
     }
     p.segmax = segmax;
-    p.ws_bytes = (size_t)p.G * segmax * p.mt * (p.nt * 8) * sizeof(double);
+    p.ws_bytes = (size_t)p.G * segmax * p.ks * p.mt * (p.nt * 8) * sizeof(double);
   }
   if (p.col) {
     p.u_bytes = (size_t)d->Q * ((d->R + 1) / 2 * 2) * sizeof(double);
@@ -497,48 +558,49 @@ Plan plan_of(const eb_contract_desc* d) {
   return p;
 }
 
-template <bool COL, bool BATCHED, int NW, int WM, int NT, int KD>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
-  using T = Tile<COL, NW * WM, NT, KD>;
-  auto kern = contract_kernel<COL, BATCHED, NW, WM, NT, KD>;
+  using T = Tile<COL, NWM * WM, NT, KD>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, NT>;
   static bool attr = false;
   if (!attr) {
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
     attr = true;
   }
-  kern<<<prm.G, (NW + 1) * 32, T::kSmem, st>>>(xm, um, prm);
+  kern<<<prm.G, (NWM * KS + 1) * 32, T::kSmem, st>>>(xm, um, prm);
   EB_CUDA(cudaGetLastError());
 }
 
-template <bool COL, bool BATCHED, int WM>
+// Column-tile count dispatch over [NT_LO, NT_HI] (configurations whose
+// accumulators would not fit are never instantiated).
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT_LO, int NT_HI>
 void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
                  cudaStream_t st) {
-  switch (nt) {
-    case 1: return launch_t<COL, BATCHED, 4, WM, 1, 32>(xm, um, prm, st);
-    case 2: return launch_t<COL, BATCHED, 4, WM, 2, 32>(xm, um, prm, st);
-    case 3: return launch_t<COL, BATCHED, 4, WM, 3, 32>(xm, um, prm, st);
-    case 4: return launch_t<COL, BATCHED, 4, WM, 4, 32>(xm, um, prm, st);
-    case 5: return launch_t<COL, BATCHED, 4, WM, 5, 32>(xm, um, prm, st);
-    case 6: return launch_t<COL, BATCHED, 4, WM, 6, 32>(xm, um, prm, st);
-    case 7: return launch_t<COL, BATCHED, 4, WM, 7, 32>(xm, um, prm, st);
-    case 8: return launch_t<COL, BATCHED, 4, WM, 8, 32>(xm, um, prm, st);
+  if constexpr (NT_LO <= NT_HI) {
+    if (nt == NT_LO) return launch_t<COL, BATCHED, NWM, WM, KS, KD, NT_LO>(xm, um, prm, st);
+    return dispatch_nt<COL, BATCHED, NWM, WM, KS, KD, NT_LO + 1, NT_HI>(nt, xm, um, prm, st);
+  } else {
+    throw InvalidError("eb_contract: unsupported column tile count");
   }
-  throw InvalidError("eb_contract: unsupported column tile count");
+}
+
+template <bool COL>
+void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
+                     const ContractParams& prm, cudaStream_t st) {
+  if (p.wm == 16) return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 8>(nt, xm, um, prm, st);
+  if (p.ks == 2) return dispatch_nt<COL, false, 4, 32, 2, 32, 1, 4>(nt, xm, um, prm, st);
+  return dispatch_nt<COL, false, 2, 32, 4, 64, 1, 4>(nt, xm, um, prm, st);
 }
 
 void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                     const ContractParams& prm, cudaStream_t st) {
-  if (p.col && p.batched) {
-    if (p.wm == 32) dispatch_nt<true, true, 32>(nt, xm, um, prm, st);
-    else dispatch_nt<true, true, 16>(nt, xm, um, prm, st);
-  } else if (p.col) {
-    if (p.wm == 32) dispatch_nt<true, false, 32>(nt, xm, um, prm, st);
-    else dispatch_nt<true, false, 16>(nt, xm, um, prm, st);
-  } else {
-    if (p.wm == 32) dispatch_nt<false, false, 32>(nt, xm, um, prm, st);
-    else dispatch_nt<false, false, 16>(nt, xm, um, prm, st);
+  if (p.batched) {
+    if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 8>(nt, xm, um, prm, st);
+    return dispatch_nt<true, true, 4, 16, 1, 32, 1, 8>(nt, xm, um, prm, st);
   }
+  if (p.col) return dispatch_reduce<true>(p, nt, xm, um, prm, st);
+  return dispatch_reduce<false>(p, nt, xm, um, prm, st);
 }
 
 void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -619,7 +681,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
       const int np = nt * 8;
       const int64_t n = d->M * np;
       reduce_partials_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(
-          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.O * p.KC, p.items, p.G,
+          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks, p.O * p.KC, p.items, p.G,
           p.segmax);
       EB_CUDA(cudaGetLastError());
     }

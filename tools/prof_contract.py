@@ -1,0 +1,50 @@
+"""Run one eb_contract configuration a few times (for ncu captures)."""
+import ctypes, sys
+import torch
+sys.path.insert(0, "/root/repo")
+from paper_2206_08301_b200 import _capi as C
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2m0"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = torch.device("cuda:0")
+
+
+def fac(t):
+    return C.Factor(t.data_ptr(), t.shape[0], t.shape[1])
+
+
+def desc(variant, P, M, Q, L, R, X, U, pre, mid, out, mode=C.EB_REDUCE):
+    d = C.ContractDesc()
+    d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = variant, mode, P, M, Q, L, R
+    d.X, d.U, d.ldu = X.data_ptr(), U.data_ptr(), U.shape[1]
+    d.n_pre = len(pre)
+    for i, f in enumerate(pre): d.pre[i] = fac(f)
+    d.n_mid = len(mid)
+    for i, f in enumerate(mid): d.mid[i] = fac(f)
+    d.out = out.data_ptr()
+    return d
+
+
+r = lambda *s: torch.rand(*s, dtype=torch.float64, device=dev)
+if cfg.startswith("c2"):
+    X = r(1024, 1024, 1024); A, B, Cm = r(1024, 32), r(1024, 32), r(1024, 32)
+    out = torch.zeros(1024, 32, dtype=torch.float64, device=dev)
+    d = {"c2m0": lambda: desc(C.EB_ROW, 1, 1024, 1024, 1024, 32, X, Cm, [], [B], out),
+         "c2m1": lambda: desc(C.EB_ROW, 1024, 1024, 1, 1024, 32, X, Cm, [A], [], out),
+         "c2m2": lambda: desc(C.EB_COL, 1024, 1024, 1024, 0, 32, X, B, [A], [], out)}[cfg]()
+elif cfg == "c1":
+    X = r(512, 512, 512); B, Cm = r(512, 24), r(512, 24)
+    out = torch.zeros(512, 24, dtype=torch.float64, device=dev)
+    d = desc(C.EB_ROW, 1, 512, 512, 512, 24, X, Cm, [], [B], out)
+elif cfg == "c3":
+    X = r(64, 64, 64, 64, 64); F = [r(64, 24) for _ in range(4)]
+    out = torch.zeros(64, 24, dtype=torch.float64, device=dev)
+    d = desc(C.EB_ROW, 1, 64, 64 ** 3, 64, 24, X, F[3], [], F[:3], out)
+L = C.lib()
+wsb = L.eb_contract_workspace(ctypes.byref(d))
+ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+for _ in range(reps):
+    C.check(L.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wsb, st))
+torch.cuda.synchronize()
+print("done", cfg)
