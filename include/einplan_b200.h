@@ -98,12 +98,49 @@ int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst
                 const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
                 const int64_t* ox_lo, void* stream);
 
+/* Any dense einsum with up to 8 operands, evaluated on the device (used for
+ * run(..., verify) on the GPU: the reference compares against naive_evaluate,
+ * executor.cpp:255-261). */
+int eb_einsum_generic(int n_ops, const char* const* in_indices, const char* out_indices,
+                      const int64_t* ext, const double* const* ops, double* out, void* stream);
+
 /* Seeded input generation identical to random_tensor (tensor.cpp:55-63):
  * fills host memory with n values of the mt19937_64(seed) stream starting at
- * element `skip`, using `threads` host threads (the stream is advanced by
- * jump-free re-seeding per chunk boundary, so threads > 1 only pays off for
- * large n). */
+ * element `skip` of that stream. */
 void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip);
+
+void eb_free(void* p);
+
+/* Host-only planning: plan_report(make_pipeline(...)) as einplan/v1 JSON
+ * (schedule.cpp:72-80, report.cpp:194-199).  No device needed. */
+int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                 int include_messages, char** json_out);
+
+/* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------
+ * rank < 0: all `procs` ranks are virtual and resident on the current device
+ *           (reductions = eb_group_sum, redistribution = eb_copy_box);
+ * rank >= 0: this process is rank `rank` of `procs`, one GPU per process,
+ *           collectives over NCCL (nccl_id = 128 bytes from
+ *           eb_nccl_unique_id on rank 0, broadcast by the caller). */
+typedef struct eb_exec eb_exec;
+
+int eb_nccl_unique_id(void* out128);
+int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                   int64_t rank, const void* nccl_id, void* stream, eb_exec** out);
+void eb_exec_destroy(eb_exec* h);
+/* scatter (executor.cpp:48-65): host global inputs -> this process's blocks */
+int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
+/* all terms: local contractions + reductions + redistributions, device only */
+int eb_exec_run(eb_exec* h);
+/* gather canonical output blocks to host (virtual mode, or rank 0) */
+int eb_exec_gather(eb_exec* h, double* host_out);
+int64_t eb_exec_output_elems(eb_exec* h);
+/* out8 = {allreduce_volume, redistribute_volume, max_rank_sent,
+ *         fused MTTKRP launches, TTM/GEMM launches, generic launches,
+ *         tree flops, terms} of the last run */
+int eb_exec_stats(eb_exec* h, int64_t* out8);
+/* run_report JSON of the last run (output sum from host_out, may be NULL) */
+int eb_exec_report_json(eb_exec* h, const double* host_out, char** json_out);
 
 #ifdef __cplusplus
 } /* extern "C" */

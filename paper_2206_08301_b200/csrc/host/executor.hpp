@@ -1,0 +1,143 @@
+// GPU schedule executor (see executor.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "einplan_b200.h"
+#include "einplan_host.hpp"
+
+namespace einplan {
+namespace gpu {
+
+// One rank's block of a tensor in device memory (row-major, global base).
+struct DevBlock {
+  double* ptr = nullptr;
+  std::vector<std::int64_t> shape;
+  std::vector<std::int64_t> base;
+  std::int64_t size() const {
+    std::int64_t n = 1;
+    for (auto d : shape) n *= d;
+    return n;
+  }
+};
+
+// Stream-ordered device allocations released together.
+class DeviceArena {
+ public:
+  ~DeviceArena();
+  double* alloc(std::int64_t elems, cudaStream_t st, bool zero);
+  void release(cudaStream_t st);
+
+ private:
+  std::vector<void*> live_;
+};
+
+// How ranks exchange data: all virtual ranks on one device, or one rank per
+// process over NCCL.
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual bool owns(std::int64_t rank) const = 0;
+  virtual bool is_virtual() const = 0;
+  virtual std::int64_t allreduce(const TensorPlacement& place, const ReductionGroup& grp,
+                                 std::vector<DevBlock>& blocks,
+                                 std::vector<std::int64_t>& per_rank_sent, cudaStream_t st) = 0;
+  virtual void redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
+                            std::vector<DevBlock>& dst, cudaStream_t st) = 0;
+  virtual void gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
+                              cudaStream_t st) = 0;
+};
+
+class VirtualTransport final : public Transport {
+ public:
+  explicit VirtualTransport(std::int64_t procs) : procs_(procs) {}
+  bool owns(std::int64_t r) const override { return r >= 0 && r < procs_; }
+  bool is_virtual() const override { return true; }
+  std::int64_t allreduce(const TensorPlacement& place, const ReductionGroup& grp,
+                         std::vector<DevBlock>& blocks, std::vector<std::int64_t>& per_rank_sent,
+                         cudaStream_t st) override;
+  void redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
+                    std::vector<DevBlock>& dst, cudaStream_t st) override;
+  void gather_to_root(const TensorPlacement&, std::vector<DevBlock>&, cudaStream_t) override {}
+
+ private:
+  std::int64_t procs_;
+};
+
+#ifdef EB_HAVE_NCCL
+class NcclTransport final : public Transport {
+ public:
+  NcclTransport(const void* unique_id, std::int64_t nranks, std::int64_t rank);
+  ~NcclTransport() override;
+  bool owns(std::int64_t r) const override { return r == rank_; }
+  bool is_virtual() const override { return false; }
+  std::int64_t allreduce(const TensorPlacement& place, const ReductionGroup& grp,
+                         std::vector<DevBlock>& blocks, std::vector<std::int64_t>& per_rank_sent,
+                         cudaStream_t st) override;
+  void redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
+                    std::vector<DevBlock>& dst, cudaStream_t st) override;
+  void gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
+                      cudaStream_t st) override;
+
+ private:
+  std::int64_t rank_, nranks_;
+  void* world_ = nullptr;
+  std::map<std::string, void*> split_;
+  DeviceArena arena_;
+};
+#endif
+
+class ScheduleExecutor {
+ public:
+  ScheduleExecutor(Pipeline pipe, Transport* transport, cudaStream_t stream);
+  ~ScheduleExecutor();
+
+  // scatter (executor.cpp:48-65): every owned rank's input blocks to device.
+  void stage_inputs(const std::vector<const double*>& global_inputs);
+  // All terms: local contractions, reductions, redistributions (device only).
+  void execute();
+  // Canonical output blocks to host (virtual, or rank 0 over NCCL).
+  void gather(double* host_out);
+  void verify(const std::vector<const double*>& global_inputs, const double* host_out,
+              double tol, SimulationReport& rep);
+
+  const CommStats& comm() const { return comm_; }
+  const Pipeline& pipeline() const { return pipe_; }
+  std::vector<std::int64_t> output_shape() const;
+  int launches_fused() const { return launches_fused_; }
+  int launches_ttm() const { return launches_ttm_; }
+  int launches_generic() const { return launches_generic_; }
+  cudaStream_t stream() const { return stream_; }
+
+ private:
+  std::int64_t local_lo(const TermPlan& t, char c, std::int64_t rank) const;
+  std::int64_t local_len(const TermPlan& t, char c, std::int64_t rank) const;
+  void copy_block_h2d(const double* global, const std::vector<std::int64_t>& gshape,
+                      const DevBlock& b);
+  const RedistRecord* find_redist(int to_term, const std::string& t) const;
+  void* workspace(std::size_t bytes);
+  DevBlock new_block(const TermPlan& term, const std::string& idx, std::int64_t rank, bool zero);
+  bool try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
+                        const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
+  DevBlock run_step(const TermPlan& term, int sid, std::int64_t rank,
+                    const std::map<std::string, const DevBlock*>& at_hand);
+
+  Pipeline pipe_;
+  Transport* transport_;
+  cudaStream_t stream_;
+  std::vector<std::int64_t> owned_;
+  std::map<std::pair<int, std::string>, std::vector<DevBlock>> inputs_;
+  std::map<std::pair<int, std::string>, std::vector<DevBlock>> store_;
+  DeviceArena input_arena_, run_arena_;
+  void* workspace_ = nullptr;
+  std::size_t workspace_bytes_ = 0;
+  CommStats comm_;
+  int launches_fused_ = 0, launches_ttm_ = 0, launches_generic_ = 0;
+};
+
+}  // namespace gpu
+}  // namespace einplan

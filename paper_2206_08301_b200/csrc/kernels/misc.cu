@@ -1,0 +1,245 @@
+// Device kernels for the non-hot-path parts of a term on B200:
+//   * eb_step_generic / eb_einsum_generic — any dense einsum (<= 8 operands)
+//     on row-major device blocks: the GPU stand-in for naive_evaluate
+//     (proj/src/evaluate.cpp:7-63) for step shapes the DMMA contraction
+//     kernel does not take (GEMM chains, KRP, OUTER, ELEMENTWISE), and the
+//     device-side verification of run(..., verify) (executor.cpp:255-261);
+//   * eb_group_sum — the in-device reduction-group sum of virtual ranks
+//     (executor.cpp:80-108: acc from 0.0, ascending rank, written to all);
+//   * eb_copy_box — one redistribution message / scatter / gather box
+//     (redistribute.cpp:152-183, executor.cpp:17-78).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../host/status.hpp"
+#include "einplan_b200.h"
+
+namespace eb {
+
+constexpr int kMaxOps = 8;
+constexpr int kMaxSym = 24;
+
+struct EinsumParams {
+  int nops;
+  int nfree, nsum;
+  int64_t free_ext[kMaxSym];
+  int64_t sum_ext[kMaxSym];
+  int64_t free_stride[kMaxOps][kMaxSym];  // operand stride per free (output) symbol
+  int64_t sum_stride[kMaxOps][kMaxSym];   // operand stride per summed symbol
+  const double* ops[kMaxOps];
+  double* out;
+  int64_t out_n;
+  int64_t sum_n;
+};
+
+// One warp per output element: lanes stride over the summed index space and
+// combine with a fixed butterfly (deterministic).
+__global__ void einsum_generic_kernel(const EinsumParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < p.out_n;
+       e += warps) {
+    int64_t base[kMaxOps];
+    for (int k = 0; k < p.nops; ++k) base[k] = 0;
+    int64_t rem = e;
+    for (int f = p.nfree - 1; f >= 0; --f) {
+      const int64_t c = rem % p.free_ext[f];
+      rem /= p.free_ext[f];
+      for (int k = 0; k < p.nops; ++k) base[k] += c * p.free_stride[k][f];
+    }
+    double acc = 0.0;
+    for (int64_t s = lane; s < p.sum_n; s += 32) {
+      int64_t off[kMaxOps];
+      for (int k = 0; k < p.nops; ++k) off[k] = base[k];
+      int64_t r = s;
+      for (int d = p.nsum - 1; d >= 0; --d) {
+        const int64_t c = r % p.sum_ext[d];
+        r /= p.sum_ext[d];
+        for (int k = 0; k < p.nops; ++k) off[k] += c * p.sum_stride[k][d];
+      }
+      double v = p.ops[0][off[0]];
+      for (int k = 1; k < p.nops; ++k) v *= p.ops[k][off[k]];
+      acc += v;
+    }
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+    if (lane == 0) p.out[e] = acc;
+  }
+}
+
+struct GroupParams {
+  double* members[64];
+  int n;
+  int64_t len;
+};
+
+__global__ void group_sum_kernel(const GroupParams g) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int m = 0; m < g.n; ++m) acc += g.members[m][i];
+    for (int m = 0; m < g.n; ++m) g.members[m][i] = acc;
+  }
+}
+
+constexpr int kMaxDim = 16;
+struct BoxParams {
+  int nd;
+  int64_t len[kMaxDim];
+  int64_t sstride[kMaxDim], dstride[kMaxDim];
+  int64_t soff, doff;
+  int64_t total;
+  const double* src;
+  double* dst;
+};
+
+__global__ void copy_box_kernel(const BoxParams b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b.total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, so = b.soff, dof = b.doff;
+    for (int d = b.nd - 1; d >= 0; --d) {
+      const int64_t c = r % b.len[d];
+      r /= b.len[d];
+      so += c * b.sstride[d];
+      dof += c * b.dstride[d];
+    }
+    b.dst[dof] = b.src[so];
+  }
+}
+
+unsigned grid_for(int64_t n, int threads) {
+  const int64_t b = (n + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+std::vector<int64_t> row_major_strides(const std::string& idx, const int64_t* ext) {
+  std::vector<int64_t> st(idx.size(), 1);
+  for (int d = (int)idx.size() - 2; d >= 0; --d)
+    st[(size_t)d] = st[(size_t)d + 1] * ext[(unsigned char)idx[(size_t)d + 1]];
+  return st;
+}
+
+void einsum_launch(const std::vector<std::string>& in_idx, const std::string& out_idx,
+                   const int64_t* ext, const double* const* ops, double* out,
+                   cudaStream_t st) {
+  EinsumParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.nops = (int)in_idx.size();
+  if (p.nops < 1 || p.nops > kMaxOps) throw InvalidError("einsum_generic: 1..8 operands");
+  std::string free_syms = out_idx, sum_syms;
+  for (const auto& s : in_idx)
+    for (char c : s)
+      if (free_syms.find(c) == std::string::npos && sum_syms.find(c) == std::string::npos)
+        sum_syms.push_back(c);
+  if ((int)free_syms.size() > kMaxSym || (int)sum_syms.size() > kMaxSym)
+    throw InvalidError("einsum_generic: too many symbols");
+  p.nfree = (int)free_syms.size();
+  p.nsum = (int)sum_syms.size();
+  p.out_n = 1;
+  for (int f = 0; f < p.nfree; ++f) {
+    p.free_ext[f] = ext[(unsigned char)free_syms[(size_t)f]];
+    p.out_n *= p.free_ext[f];
+  }
+  p.sum_n = 1;
+  for (int d = 0; d < p.nsum; ++d) {
+    p.sum_ext[d] = ext[(unsigned char)sum_syms[(size_t)d]];
+    p.sum_n *= p.sum_ext[d];
+  }
+  for (int k = 0; k < p.nops; ++k) {
+    const std::string& idx = in_idx[(size_t)k];
+    const auto st_k = row_major_strides(idx, ext);
+    for (size_t d = 0; d < idx.size(); ++d) {
+      const char c = idx[d];
+      const auto f = free_syms.find(c);
+      if (f != std::string::npos) p.free_stride[k][f] += st_k[d];
+      else p.sum_stride[k][sum_syms.find(c)] += st_k[d];
+    }
+    if (!ops[k]) throw InvalidError("einsum_generic: null operand");
+    p.ops[k] = ops[k];
+  }
+  for (char c : out_idx)
+    if (std::none_of(in_idx.begin(), in_idx.end(),
+                     [c](const std::string& s) { return s.find(c) != std::string::npos; }))
+      throw InvalidError("einsum_generic: output symbol absent from inputs");
+  p.out = out;
+  if (p.out_n == 0) return;
+  const int threads = 256;
+  const int64_t warps_needed = p.out_n;
+  einsum_generic_kernel<<<grid_for(warps_needed * 32, threads), threads, 0, st>>>(p);
+  EB_CUDA(cudaGetLastError());
+}
+
+}  // namespace eb
+
+extern "C" int eb_step_generic(const char* lhs, const char* rhs, const char* out,
+                               const int64_t* ext, const double* lhs_ptr, const double* rhs_ptr,
+                               double* out_ptr, void* stream) {
+  return eb::guard([&] {
+    if (!lhs || !out || !ext) throw eb::InvalidError("eb_step_generic: null argument");
+    std::vector<std::string> in{lhs};
+    std::vector<const double*> ops{lhs_ptr};
+    if (rhs && rhs[0]) {
+      in.emplace_back(rhs);
+      ops.push_back(rhs_ptr);
+    }
+    eb::einsum_launch(in, out, ext, ops.data(), out_ptr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" int eb_einsum_generic(int nops, const char* const* in_indices, const char* out_indices,
+                                 const int64_t* ext, const double* const* ops, double* out,
+                                 void* stream) {
+  return eb::guard([&] {
+    if (nops < 1 || nops > eb::kMaxOps) throw eb::InvalidError("eb_einsum_generic: 1..8 operands");
+    std::vector<std::string> in;
+    for (int k = 0; k < nops; ++k) in.emplace_back(in_indices[k]);
+    eb::einsum_launch(in, out_indices, ext, ops, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" int eb_group_sum(double* const* members, int n_members, int64_t n, void* stream) {
+  return eb::guard([&] {
+    if (n_members < 1 || n_members > 64) throw eb::InvalidError("eb_group_sum: 1..64 members");
+    eb::GroupParams g;
+    std::memset(&g, 0, sizeof(g));
+    g.n = n_members;
+    g.len = n;
+    for (int m = 0; m < n_members; ++m) g.members[m] = members[m];
+    if (n == 0 || n_members == 1) return;
+    eb::group_sum_kernel<<<eb::grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g);
+    EB_CUDA(cudaGetLastError());
+  });
+}
+
+extern "C" int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst,
+                           const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
+                           const int64_t* ox_lo, void* stream) {
+  return eb::guard([&] {
+    if (nd < 0 || nd > eb::kMaxDim) throw eb::InvalidError("eb_copy_box: bad rank");
+    eb::BoxParams b;
+    std::memset(&b, 0, sizeof(b));
+    b.nd = nd;
+    b.src = src;
+    b.dst = dst;
+    int64_t ss = 1, ds = 1;
+    b.total = 1;
+    for (int d = nd - 1; d >= 0; --d) {
+      b.len[d] = oy_hi[d] - oy_lo[d];
+      if (b.len[d] <= 0) return;
+      b.sstride[d] = ss;
+      b.dstride[d] = ds;
+      b.soff += oy_lo[d] * ss;
+      b.doff += ox_lo[d] * ds;
+      ss *= src_shape[d];
+      ds *= dst_shape[d];
+      b.total *= b.len[d];
+    }
+    eb::copy_box_kernel<<<eb::grid_for(b.total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    EB_CUDA(cudaGetLastError());
+  });
+}
