@@ -1,7 +1,8 @@
-"""ctypes bindings of the in-tree libeinplan_b200.so (C ABI in include/).
+"""ctypes bindings of the in-tree libeinplan_b200.so (C ABIs in include/).
 
-The product path: every compute call goes to the CUDA library; if it cannot
-be loaded the import fails loudly (there is no CPU fallback).
+This is the product path: every compute call goes to the CUDA library.  If
+the library cannot be loaded the import of the call site fails loudly —
+there is no CPU fallback anywhere in this package.
 """
 from __future__ import annotations
 
@@ -12,6 +13,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libeinplan_b200.so")
 
 _dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
 
 
 class Factor(ctypes.Structure):
@@ -33,13 +36,37 @@ class ContractDesc(ctypes.Structure):
 EB_ROW, EB_COL = 0, 1
 EB_REDUCE, EB_BATCHED = 0, 1
 
+# einplan_status (include/einplan/einplan.h)
+EINPLAN_OK, EINPLAN_E_VERIFY, EINPLAN_E_PARSE, EINPLAN_E_INFEASIBLE = 0, 1, 2, 3
+EINPLAN_E_GRID, EINPLAN_E_RESOURCE, EINPLAN_E_INVALID, EINPLAN_E_INTERNAL = 4, 5, 6, 7
+
+# Every symbol include/*.h declares (checked by tests/test_capi_load.py).
+EXPORTS = [
+    "einplan_version", "einplan_status_name", "einplan_last_error", "einplan_free",
+    "einplan_session_create", "einplan_session_destroy", "einplan_bound_json",
+    "einplan_plan_json", "einplan_run_json", "einplan_bench_json",
+    "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_step_generic",
+    "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
+    "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_destroy", "eb_exec_stage",
+    "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
+    "eb_exec_report_json",
+]
+
 _lib = None
 
 
 class EinplanError(RuntimeError):
+    """A nonzero status from the C ABI (status carries the code)."""
+
     def __init__(self, status: int, msg: str):
         super().__init__(f"[{status}] {msg}")
         self.status = status
+
+
+def _sig(L, name, res, args):
+    f = getattr(L, name)
+    f.restype = res
+    f.argtypes = args
 
 
 def lib():
@@ -49,16 +76,50 @@ def lib():
             raise ImportError(f"{LIB_PATH} missing: build it with "
                               "`python -m paper_2206_08301_b200.build` (no CPU fallback exists)")
         L = ctypes.CDLL(LIB_PATH)
-        L.eb_last_error.restype = ctypes.c_char_p
-        L.eb_contract_workspace.argtypes = [ctypes.POINTER(ContractDesc)]
-        L.eb_contract_workspace.restype = ctypes.c_size_t
-        L.eb_contract.argtypes = [ctypes.POINTER(ContractDesc), ctypes.c_void_p, ctypes.c_size_t,
-                                  ctypes.c_void_p]
-        L.eb_contract.restype = ctypes.c_int
+        c = ctypes.c_char_p
+        _sig(L, "einplan_version", c, [])
+        _sig(L, "einplan_status_name", c, [ctypes.c_int])
+        _sig(L, "einplan_last_error", c, [])
+        _sig(L, "einplan_free", None, [_vp])
+        _sig(L, "einplan_session_create", ctypes.c_int, [c, c, ctypes.POINTER(_vp)])
+        _sig(L, "einplan_session_destroy", None, [_vp])
+        _sig(L, "einplan_bound_json", ctypes.c_int, [_vp, ctypes.c_double, ctypes.POINTER(_vp)])
+        _sig(L, "einplan_plan_json", ctypes.c_int,
+             [_vp, _i64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(_vp)])
+        _sig(L, "einplan_run_json", ctypes.c_int,
+             [_vp, _i64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int, c, c, ctypes.POINTER(_vp)])
+        _sig(L, "einplan_bench_json", ctypes.c_int,
+             [ctypes.c_double, _i64, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_vp)])
+        _sig(L, "eb_last_error", c, [])
+        _sig(L, "eb_build_info", c, [])
+        _sig(L, "eb_contract_workspace", ctypes.c_size_t, [ctypes.POINTER(ContractDesc)])
+        _sig(L, "eb_contract", ctypes.c_int,
+             [ctypes.POINTER(ContractDesc), _vp, ctypes.c_size_t, _vp])
+        _sig(L, "eb_random_fill_host", None, [_dp, _i64, ctypes.c_uint64, _i64])
+        _sig(L, "eb_free", None, [_vp])
+        _sig(L, "eb_plan_json", ctypes.c_int,
+             [c, c, _i64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(_vp)])
+        _sig(L, "eb_nccl_unique_id", ctypes.c_int, [_vp])
+        _sig(L, "eb_exec_create", ctypes.c_int,
+             [c, c, _i64, ctypes.c_double, _i64, _vp, _vp, ctypes.POINTER(_vp)])
+        _sig(L, "eb_exec_destroy", None, [_vp])
+        _sig(L, "eb_exec_stage", ctypes.c_int, [_vp, ctypes.POINTER(_dp)])
+        _sig(L, "eb_exec_run", ctypes.c_int, [_vp])
+        _sig(L, "eb_exec_gather", ctypes.c_int, [_vp, _dp])
+        _sig(L, "eb_exec_output_elems", _i64, [_vp])
+        _sig(L, "eb_exec_stats", ctypes.c_int, [_vp, ctypes.POINTER(_i64)])
+        _sig(L, "eb_exec_report_json", ctypes.c_int, [_vp, _dp, ctypes.POINTER(_vp)])
         _lib = L
     return _lib
 
 
 def check(status: int):
+    """Raise EinplanError for a nonzero eb_status."""
     if status != 0:
         raise EinplanError(status, lib().eb_last_error().decode())
+
+
+def take_string(p: ctypes.c_void_p, free=None) -> str:
+    s = ctypes.string_at(p).decode()
+    (free or lib().einplan_free)(p)
+    return s
