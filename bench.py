@@ -1,0 +1,482 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Deinsum hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl b200|reference]
+
+Workload (default C2 = BASELINE configs[1], the config the metric is quoted
+on that fits one GPU): the order-3 CP-ALS MTTKRP sweep — mode-0, mode-1 and
+mode-2 MTTKRP of a dense fp64 1024^3 tensor with 1024x32 factors — each mode
+planned by the reference's pipeline (make_pipeline, S = 1024) on the
+processor grid for N ranks and executed by the GPU executor.  One step = the
+three modes.  N > 1 runs one process per GPU (torchrun), each rank the
+reference grid's rank r, partial outputs summed by NCCL allreduce on
+ncclCommSplit sub-communicators; the JSON line is printed by rank 0 with the
+max-over-ranks device time.
+
+`value` (device-timed, inputs resident in HBM) = reference tree flops of the
+step / time.  `e2e` = the same metric through the C ABI with host buffers
+(pinned at N = 1): per mode eb_exec_stage (H2D) + eb_exec_run + eb_exec_gather
+(D2H), wall clock with device syncs on both sides.  `--impl reference` times
+the reference implementation itself (oracle/_ref, compiled from the
+reference's sources) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+FP64_PEAK_TFLOPS = 37.05   # measured DMMA.8x8x4 peak on this pool's B200 (profiles/fp64_peak_r01.jsonl)
+HBM_READ_GBS = 7182.5      # measured read-only stream (same file)
+
+
+def _load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+# --------------------------------------------------------------- configs --
+
+def workload(name: str, P: int):
+    """(label, [(einsum, extents, input-builder)], scaling, l2_note)."""
+    from tests.configs import CONFIGS, C2_FACTOR_SEED
+    import paper_2206_08301_b200 as eb
+    c = CONFIGS[name]
+    ext = c["extents"](P)
+
+    def seeded_builder(e, shared_seed=None):
+        ins, _ = e.split("->")[0].split(","), None
+
+        def build(pinned):
+            out = []
+            for k, t in enumerate(ins):
+                shape = tuple(ext[s] for s in t)
+                seed = k if shared_seed is None else (0 if k == 0 else C2_FACTOR_SEED[t[0]])
+                out.append(_fill(shape, seed, pinned and k == 0))
+            return out
+        return build
+
+    modes = []
+    for e in c["einsums"]:
+        modes.append((e, ext, seeded_builder(e, shared_seed=(name == "C2"))))
+    label = {
+        "C1": "C1: order-3 MTTKRP mode-0, X 512^3, R=24",
+        "C2": "C2: order-3 CP-ALS MTTKRP sweep (modes 0,1,2), X 1024^3 fp64, factors 1024x32",
+        "C3": "C3: order-5 MTTKRP mode-0, X 64^5, R=24",
+        "C4": "C4: order-3 TTMc mode-0, X 1024^3, U1/U2 1024x64 (binary chain)",
+        "C5": "C5: order-5 TTMc mode-0, X (64P)x64^4, factors 64x16 (weak scaling)",
+    }[name]
+    scaling = "weak" if name == "C5" else "strong"
+    return label, modes, scaling
+
+
+_pinned_keep = []
+
+
+def _fill(shape, seed, pinned):
+    import paper_2206_08301_b200 as eb
+    from paper_2206_08301_b200 import _capi
+    n = int(np.prod(shape))
+    if pinned:
+        import torch
+        t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        _pinned_keep.append(t)
+        arr = t.numpy()
+    else:
+        arr = np.empty(n, dtype=np.float64)
+    _capi.lib().eb_random_fill_host(arr.ctypes.data_as(_capi._dp), n, seed, 0)
+    return arr.reshape(shape)
+
+
+# ---------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------- reference arm --
+
+def _ref_sample_step(threads: int, rows: int):
+    """One bounded sample of the C2 sweep on the reference implementation:
+    `threads` concurrent reference run() calls (P=1), each on its own slab of
+    `rows` i-rows of X for all three modes.  Returns (flops, seconds)."""
+    import oracle
+    from tests.configs import CONFIGS, c2_inputs
+    c = CONFIGS["C2"]
+    work = []
+    flops_per_mode = {}
+    ext = dict(c["extents"](1))
+    ext["i"] = rows
+    for t in range(threads):
+        X = oracle.random_tensor((rows, 1024, 1024), 100 + t)
+        per_mode = []
+        for mode, e in enumerate(c["einsums"]):
+            ins, _ = oracle.parse(e)
+            ops = [X] + [oracle.random_tensor(oracle.shape_of(s, ext), {"i": 1, "j": 2, "k": 3}[s[0]])
+                         for s in ins[1:]]
+            per_mode.append((e, ext, ops))
+            if e not in flops_per_mode:
+                flops_per_mode[e] = json.loads(oracle.ref_plan_json(e, ext, 1))["tree"]["total_flops"]
+        work.append(per_mode)
+    flops = sum(flops_per_mode[e] for per_mode in work for e, _, _ in per_mode)
+
+    def body(t):
+        for e, ext, ops in work[t]:
+            oracle.ref_run(e, ext, 1, ops)
+    ths = [threading.Thread(target=body, args=(t,)) for t in range(threads)]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return flops, time.perf_counter() - t0
+
+
+def cpu_kind():
+    import oracle
+    return "reference" if oracle.ref_available() else "port"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    if not oracle.ref_available():
+        oracle.build(ref=True)
+    if args.config != "C2":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for C2"}))
+        return 0
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, 32))
+    rows = 8
+    for _ in range(args.warmup):
+        _ref_sample_step(threads, rows)
+    tot_f, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        f, s = _ref_sample_step(threads, rows)
+        tot_f += f
+        tot_s += s
+    value = tot_f / tot_s / 1e9
+    sample = (f"C2 sweep sample per step: {threads} concurrent reference run() calls (P=1, "
+              f"single-threaded each, oracle/_ref built from the reference sources), each on an "
+              f"{rows}-row i-slab of X (X[{rows},1024,1024], all 3 modes); GFLOP/s = reference "
+              f"tree flops / wall time")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference random_tensor, mt19937_64 seed 0 / factor seeds 1,2,3)",
+        "config": {"workload": workload_label("C2"), "sample_rows_per_thread": rows,
+                   "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads,
+                         "kind": cpu_kind(), "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_label(name):
+    return {
+        "C2": "C2: order-3 CP-ALS MTTKRP sweep (modes 0,1,2), X 1024^3 fp64, factors 1024x32",
+    }.get(name, name)
+
+
+def cpu_baseline_leg():
+    """Rank 0, N = 1: the reference (or the oracle port) on a bounded sample,
+    single-threaded as the reference is (README.md:149-150)."""
+    import oracle
+    if not oracle.ref_available():
+        try:
+            oracle.build(ref=True)
+        except Exception:
+            pass
+    if oracle.ref_available():
+        f, s = _ref_sample_step(1, 16)
+        return {"value": f / s / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
+                "sample": "C2 sweep (3 modes) on X[0:16,:,:] (16 of 1024 i-rows), reference "
+                          "run() at P=1, one host thread (the reference is single-threaded); "
+                          f"{s:.1f} s of CPU work"}
+    # Port: the C restatement on a smaller slab.
+    ext = dict(i=4, j=1024, k=1024, a=32)
+    t0 = time.perf_counter()
+    fl = 0
+    for e in ("ijk,ja,ka->ia", "ijk,ia,ka->ja", "ijk,ia,ja->ka"):
+        ops = oracle.seeded_inputs(e, ext, 0)
+        oracle.naive_evaluate(e, ext, ops)
+        fl += 2 * 4 * 1024 * 1024 * 32
+    s = time.perf_counter() - t0
+    return {"value": fl / s / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": "C2 sweep on X[0:4,:,:] with the C oracle (naive_evaluate restatement)"}
+
+
+# --------------------------------------------------------------- B200 arm --
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = world
+    import paper_2206_08301_b200 as eb
+    from paper_2206_08301_b200 import _capi
+    L = _capi.lib()
+
+    label, modes, scaling = workload(args.config, P)
+    nccl_id = None
+    if world > 1:
+        obj = [eb.Executor.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.Stream()
+    execs, inputs, grids, flops_tree = [], [], [], 0
+    for e, ext, build in modes:
+        ins = build(pinned=(world == 1))
+        ex = eb.Executor(e, ext, P, 1024.0, rank if world > 1 else -1, nccl_id,
+                         stream=stream.cuda_stream)
+        ex.stage(ins)
+        execs.append(ex)
+        inputs.append(ins)
+        plan = json.loads(eb.plan_json(e, ext, P))
+        grids.append([t["grid"] for t in plan["schedule"]["terms"]])
+        flops_tree += plan["tree"]["total_flops"]
+    torch.cuda.synchronize()
+
+    def step():
+        for ex in execs:
+            ex.run()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                          int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    clocks.start()
+    time.sleep(0.3)
+    L.eb_timer_enable(1)
+    L.eb_timer_collect(None, None)
+    launches0 = L.eb_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = L.eb_launch_count() - launches0
+    kms = ctypes.c_double(0.0)
+    kn = ctypes.c_longlong(0)
+    L.eb_timer_collect(ctypes.byref(kms), ctypes.byref(kn))
+    L.eb_timer_enable(0)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = flops_tree / (ms_step * 1e-3) / 1e9
+
+    # e2e through the C ABI with host buffers.
+    e2e = None
+    if not args.no_e2e:
+        outs = [np.empty(ex_.gather().size) for ex_ in execs]
+        h2d = 0
+        for ins, ex_ in zip(inputs, execs):
+            # bytes this rank copies: its blocks of every operand
+            h2d += _staged_bytes(ex_, ins, P, rank if world > 1 else -1, eb)
+        d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
+        reps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            for ins, ex_, out in zip(inputs, execs, outs):
+                ex_.stage(ins)
+                ex_.run()
+                ex_.gather(out)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": flops_tree / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
+               "host_buffers": "pinned" if world == 1 else "pageable"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # Roofline of the dominant kernel (the fused contraction), live events.
+    kern_ms = kms.value / max(kn.value, 1)
+    per_launch_flops = flops_tree / len(execs) / P
+    achieved = per_launch_flops / (kern_ms * 1e-3) / 1e12
+    peaks = _load_peaks()
+    traffic = _traffic(args.config)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "kernel": "eb::contract_kernel (FP64 DMMA.8x8x4, TMA SWIZZLE_128B ring)",
+            "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.jsonl "
+                           "(MEASURED_PEAKS.json has no FP64 figure)",
+            "kernel_ms_per_launch": kern_ms, "kernel_launches_timed": kn.value,
+            "kernel_share_of_step": kms.value / max(ms, 1e-9),
+            "hbm_achieved_gbs": _x_bytes(modes, P) / len(execs) / (kern_ms * 1e-3) / 1e9,
+            "hbm_peak_gbs": peaks.get("hbm_gbs"),
+            "algorithmic_flops_per_launch": per_launch_flops}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference random_tensor streams (mt19937_64, seed 0 for X, "
+                "factor seeds 1/2/3), generated on the host",
+        "config": {"workload": label, "procs": P, "fast_mem": 1024, "grids": grids,
+                   "tree_flops_per_step": flops_tree,
+                   "l2": "inputs larger than L2 (X is 8.6 GB vs 126 MB L2), no flush needed"},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _x_bytes(modes, P):
+    tot = 0
+    for e, ext, _ in modes:
+        t = e.split("->")[0].split(",")[0]
+        tot += 8 * int(np.prod([ext[c] for c in t])) // P
+    return tot
+
+
+def _staged_bytes(ex, ins, P, rank, eb):
+    if P == 1:
+        return sum(a.nbytes for a in ins)
+    # Blocks of this rank: every operand is split over the grid dims it spans
+    plan = json.loads(eb.plan_json(ex.einsum, _ext_of(ex, ins), P))
+    tot = 0
+    for t in plan["schedule"]["terms"]:
+        for p in t["placements"]:
+            if p["tensor"].startswith("in"):
+                k = int(p["tensor"][2:])
+                tot += ins[k].nbytes // p["owners"]
+    return tot
+
+
+def _ext_of(ex, ins):
+    ext = {}
+    for t, a in zip(ex.einsum.split("->")[0].split(","), ins):
+        for c, n in zip(t, a.shape):
+            ext[c] = n
+    return ext
+
+
+def _traffic(config):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(config)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

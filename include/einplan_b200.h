@@ -142,6 +142,13 @@ int eb_exec_stats(eb_exec* h, int64_t* out8);
 /* run_report JSON of the last run (output sum from host_out, may be NULL) */
 int eb_exec_report_json(eb_exec* h, const double* host_out, char** json_out);
 
+/* Instrumentation: total kernel launches issued by this library; optional
+ * CUDA-event bracketing of the dominant contraction kernel on its launch
+ * stream (enable, run, then collect the summed milliseconds). */
+long long eb_launch_count(void);
+void eb_timer_enable(int on);
+int eb_timer_collect(double* total_ms, long long* launches);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

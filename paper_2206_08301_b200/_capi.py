@@ -49,7 +49,7 @@ EXPORTS = [
     "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
-    "eb_exec_report_json",
+    "eb_exec_report_json", "eb_launch_count", "eb_timer_enable", "eb_timer_collect",
 ]
 
 _lib = None
@@ -109,6 +109,10 @@ def lib():
         _sig(L, "eb_exec_output_elems", _i64, [_vp])
         _sig(L, "eb_exec_stats", ctypes.c_int, [_vp, ctypes.POINTER(_i64)])
         _sig(L, "eb_exec_report_json", ctypes.c_int, [_vp, _dp, ctypes.POINTER(_vp)])
+        _sig(L, "eb_launch_count", ctypes.c_longlong, [])
+        _sig(L, "eb_timer_enable", None, [ctypes.c_int])
+        _sig(L, "eb_timer_collect", ctypes.c_int,
+             [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)])
         _lib = L
     return _lib
 

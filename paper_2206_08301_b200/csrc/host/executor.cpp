@@ -272,6 +272,14 @@ ScheduleExecutor::ScheduleExecutor(Pipeline pipe, Transport* transport, cudaStre
   for (std::int64_t r = 0; r < procs; ++r)
     if (transport_->owns(r)) owned_.push_back(r);
   comm_.per_rank_sent.assign(static_cast<std::size_t>(procs), 0);
+  // Keep freed stream-ordered blocks in the pool: repeated execute() calls
+  // reuse them instead of returning memory to the driver at every sync.
+  int dev = 0;
+  cudaMemPool_t pool = nullptr;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    std::uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
 }
 
 ScheduleExecutor::~ScheduleExecutor() {

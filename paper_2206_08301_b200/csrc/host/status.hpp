@@ -46,3 +46,14 @@ int guard(Fn&& fn) {
 }
 
 }  // namespace eb
+
+#include <cuda_runtime.h>
+
+namespace eb {
+// Every kernel launch of the library is counted (bench.py's gpu_launches);
+// the dominant contraction kernel can additionally be bracketed by CUDA
+// events on its own stream (bench.py's live roofline timing).
+void count_launch();
+void main_kernel_begin(cudaStream_t st);
+void main_kernel_end(cudaStream_t st);
+}  // namespace eb

@@ -568,8 +568,11 @@ void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
     attr = true;
   }
+  main_kernel_begin(st);
   kern<<<prm.G, (NWM * KS + 1) * 32, T::kSmem, st>>>(xm, um, prm);
   EB_CUDA(cudaGetLastError());
+  main_kernel_end(st);
+  count_launch();
 }
 
 // Column-tile count dispatch over [NT_LO, NT_HI] (configurations whose
@@ -635,6 +638,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     pitch_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->Q, (int)d->R, ubuf,
                                                                  pitch);
     EB_CUDA(cudaGetLastError());
+    count_launch();
     const uint64_t dims[2] = {(uint64_t)d->R, (uint64_t)d->Q};
     const uint64_t str[1] = {(uint64_t)pitch * 8};
     const uint32_t box[2] = {16, (uint32_t)p.kd};
@@ -666,6 +670,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
       transpose_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->L, cols, col0,
                                                                        ubuf, lp);
       EB_CUDA(cudaGetLastError());
+      count_launch();
       const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)cols};
       const uint64_t str[1] = {(uint64_t)lp * 8};
       const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
@@ -684,6 +689,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
           part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks, p.O * p.KC, p.items, p.G,
           p.segmax);
       EB_CUDA(cudaGetLastError());
+      count_launch();
     }
   }
 }

@@ -172,6 +172,7 @@ void einsum_launch(const std::vector<std::string>& in_idx, const std::string& ou
   const int64_t warps_needed = p.out_n;
   einsum_generic_kernel<<<grid_for(warps_needed * 32, threads), threads, 0, st>>>(p);
   EB_CUDA(cudaGetLastError());
+    eb::count_launch();
 }
 
 }  // namespace eb
@@ -213,6 +214,7 @@ extern "C" int eb_group_sum(double* const* members, int n_members, int64_t n, vo
     if (n == 0 || n_members == 1) return;
     eb::group_sum_kernel<<<eb::grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g);
     EB_CUDA(cudaGetLastError());
+    eb::count_launch();
   });
 }
 
@@ -241,5 +243,6 @@ extern "C" int eb_copy_box(int nd, const double* src, const int64_t* src_shape, 
     }
     eb::copy_box_kernel<<<eb::grid_for(b.total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
     EB_CUDA(cudaGetLastError());
+    eb::count_launch();
   });
 }
