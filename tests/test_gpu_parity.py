@@ -275,3 +275,14 @@ def test_c4_two_ranks_redistribution_full_size(eb):
     ex.run()
     assert ex.stats()["redistribute_volume"] == 33554432
     _against_golden("C4", ex.gather())
+
+
+def test_reference_c_smoke_runs_on_gpu(eb):
+    """The reference's capi_smoke.c (compiled against include/einplan/einplan.h
+    and libeinplan_b200.so by tests/test_capi_load.py) runs and passes."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "_bin", "capi_smoke")
+    if not os.path.exists(exe):
+        pytest.skip("capi_smoke not built (needs the reference sources at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
