@@ -115,6 +115,20 @@ struct Cursor {
   }
 };
 
+// M += KRP[o] (.) T, then T = 0 (the deferred Khatri-Rao scale).
+template <int MI, int NT>
+__device__ __forceinline__ void fold_krp(double (&t)[MI][NT][2], double (&m)[MI][NT][2],
+                                         const double (&krow)[NT][2]) {
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      m[i][j][0] = fma(krow[j][0], t[i][j][0], m[i][j][0]);
+      m[i][j][1] = fma(krow[j][1], t[i][j][1], m[i][j][1]);
+      t[i][j][0] = t[i][j][1] = 0.0;
+    }
+}
+
 // Store one row tile's register accumulators into partial slot (sg, ks) of
 // this CTA and clear them.
 template <int MI, int NT, int MT, int WM, int KS>
@@ -133,11 +147,18 @@ __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const Co
     }
 }
 
-// Warp roles: warp NWM*KS is the producer (all 32 lanes compute the stage's
-// Khatri-Rao scale row, lane 0 issues the TMA boxes); consumer warp w owns
-// rows (w % NWM)*WM.. of the CTA tile and the 16-deep k groups g16 of each
-// stage with g16 % KS == w / NWM (k split inside the CTA; REDUCE keeps one
-// partial per k-split group, BATCHED requires KS == 1).
+// Warp roles:
+//   warp NCW       producer: lane 0 fills the stage ring with TMA boxes of X
+//                  and U; all 32 lanes write the stage's Khatri-Rao row
+//                  KRP(pre)[p] * KRP(mid)[q] (REDUCE) next to it.
+//   warps 0..NCW-1 consumers: warp w owns rows (w % NWM)*WM.. of the CTA tile
+//                  and the 16-deep k groups g16 of each stage with
+//                  g16 % KS == w / NWM.
+// REDUCE (MTTKRP) accumulates in two levels: T = sum over the k chunks of one
+// outer index o of X·U on DMMA (B fragments straight from shared memory),
+// then M += KRP[o] (.) T once per outer index — the Khatri-Rao product is a
+// per-column scale of T and is never formed.  One partial per k-split group.
+// BATCHED (TTM) requires KS == 1 and writes each (row tile, o) unit once.
 template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT>
 __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     }
     uint32_t it = 0;
     int64_t scale_o = -1;
-    double sc0 = 0.0, sc1 = 0.0;  // scale for columns lane, lane + 32
+    double sc0 = 0.0, sc1 = 0.0;  // KRP row, columns lane and lane + 32
     Cursor cur;
     cur.seek(i0, BATCHED, prm);
     for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
@@ -191,6 +212,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
       if (!BATCHED && o != scale_o) {
         scale_o = o;
         const int64_t p = COL ? o : o / prm.Q;
+#pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = lane + 32 * h;
           double v = 0.0;
@@ -204,13 +226,13 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
       for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
         const int st = it % S;
         if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
-        uint8_t* stage = sbase + st * T::kStageBytes;
         if (!BATCHED) {
-          double* sc = reinterpret_cast<double*>(stage + T::kXBytes + T::kUBytes);
+          double* sc = reinterpret_cast<double*>(sbase + st * T::kStageBytes + T::kXBytes +
+                                                 T::kUBytes);
           if (lane < NT * 8) sc[lane] = sc0;
           if (lane + 32 < NT * 8) sc[lane + 32] = sc1;
+          __syncwarp();
         }
-        __syncwarp();
         if (lane == 0) {
           const uint32_t fb = smem_addr(&full_bar[st]);
           mbar_expect_tx(fb, T::kXBytes + T::kUBytes);
@@ -241,11 +263,21 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
   // -------------------------------------------------------------- consumers
   const int wm = warp % NWM, ks = warp / NWM;
   const int g = lane >> 2, l = lane & 3;
-  double acc[MI][NT][2];
+  double acc[MI][NT][2];                 // T: this outer index (or the TTM unit)
+  double macc[BATCHED ? 1 : MI][NT][2];  // M: the row tile's MTTKRP partial
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (!BATCHED) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) macc[i][j][0] = macc[i][j][1] = 0.0;
+  }
+  double krow[NT][2];  // KRP scale of the current outer index, C-fragment columns
+#pragma unroll
+  for (int j = 0; j < NT; ++j) krow[j][0] = krow[j][1] = 0.0;
 
   // Per-lane byte offsets inside a 128-B swizzled row for the 4 k-steps of
   // a 16-deep group (see the header comment for the bank argument).
@@ -260,14 +292,14 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
         const uint32_t chunk = (uint32_t)((s + 4 * (l >> 1)) ^ g);
         off[s][h] = g * 128 + chunk * 16 + (l & 1) * 8;
       } else {
-        const int krow = 2 * l + (s & 1) + 8 * (s >> 1);
-        const uint32_t chunk = (uint32_t)((4 * h + (g >> 1)) ^ (krow & 7));
-        off[s][h] = krow * 128 + chunk * 16 + (g & 1) * 8;
+        const int kr = 2 * l + (s & 1) + 8 * (s >> 1);
+        const uint32_t chunk = (uint32_t)((4 * h + (g >> 1)) ^ (kr & 7));
+        off[s][h] = kr * 128 + chunk * 16 + (g & 1) * 8;
       }
     }
   }
 
-  int64_t cur_mt = -1;
+  int64_t cur_mt = -1, cur_o = -1;
   int seg = -1;
   uint32_t it = 0;
 
@@ -277,22 +309,30 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     const int64_t mt = cur.mt, o = cur.o;
     const int64_t kc_begin = cur.kc;
     const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
-    if (!BATCHED && mt != cur_mt) {
-      if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(acc, prm, seg, wm, ks, g, l);
-      ++seg;
-      cur_mt = mt;
+    if constexpr (!BATCHED) if (o != cur_o || mt != cur_mt) {
+      if (cur_o >= 0) fold_krp<MI, NT>(acc, macc, krow);
+      if (mt != cur_mt) {
+        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(macc, prm, seg, wm, ks, g, l);
+        ++seg;
+        cur_mt = mt;
+      }
+      cur_o = o;
+      // the new outer index's KRP row, from the first stage that carries it
+      const int st = it % S;
+      mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
+      const double* sc = reinterpret_cast<const double*>(sbase + st * T::kStageBytes +
+                                                         T::kXBytes + T::kUBytes);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        krow[j][0] = sc[j * 8 + 2 * l];
+        krow[j][1] = sc[j * 8 + 2 * l + 1];
+      }
     }
     for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
       const int st = it % S;
       mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
       const uint8_t* xs = sbase + st * T::kStageBytes;
       const uint8_t* us = xs + T::kXBytes;
-      double scale[NT];
-      if (!BATCHED) {
-        const double* sc = reinterpret_cast<const double*>(us + T::kUBytes);
-#pragma unroll
-        for (int j = 0; j < NT; ++j) scale[j] = sc[j * 8 + g];
-      }
 #pragma unroll
       for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
 #pragma unroll
@@ -315,8 +355,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
             o_b = b16 * NT * 8 * 128 + j * 8 * 128 + off[s][0];
           else
             o_b = (j >> 1) * KD * 128 + b16 * 16 * 128 + off[s][j & 1];
-          const double u = *reinterpret_cast<const double*>(us + o_b);
-          bf[j] = BATCHED ? u : u * scale[j];
+          bf[j] = *reinterpret_cast<const double*>(us + o_b);
         }
 #pragma unroll
         for (int i = 0; i < MI; ++i)
@@ -352,7 +391,12 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
       }
     }
   }
-  if (!BATCHED && cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(acc, prm, seg, wm, ks, g, l);
+  if constexpr (!BATCHED) {
+    if (cur_mt >= 0) {
+      fold_krp<MI, NT>(acc, macc, krow);
+      flush_partial<MI, NT, MT, WM, KS>(macc, prm, seg, wm, ks, g, l);
+    }
+  }
 }
 
 // Deterministic split-K finish: out[m][col0+n] = sum over CTAs (ascending),
@@ -513,19 +557,16 @@ Plan plan_of(const eb_contract_desc* d) {
   p.nt = (int)cdiv(rcols, 8);
   const int64_t rows = d->M;
   // Tile configurations (instantiated in dispatch below):
-  //   REDUCE, M >= 128 : 4 row warps x 32 rows, k split 2, 32-deep stages
-  //   REDUCE, M <  128 : 2 row warps x 32 rows, k split 4, 64-deep stages
-  //   REDUCE, R >  32  : 4 row warps x 16 rows, k split 2 (register budget:
-  //                      9 warps leave 168 registers per thread)
+  //   REDUCE, M >= 128 : 8 row warps x 16 rows, 32-deep stages
+  //   REDUCE, M <  128 : 4 row warps x 16 rows, k split 2, 32-deep stages
+  //   (two accumulator sets T and M per warp; 9 warps leave 168 registers)
   //   BATCHED          : 4 row warps x 32 (M >= 128) or 16 rows, 32-deep
   if (p.batched) {
     p.nwm = 4; p.wm = rows >= 128 ? 32 : 16; p.ks = 1; p.kd = 32;
-  } else if (p.nt > 4) {
-    p.nwm = 4; p.wm = 16; p.ks = 2; p.kd = 32;
   } else if (rows >= 128) {
-    p.nwm = 4; p.wm = 32; p.ks = 2; p.kd = 32;
+    p.nwm = 8; p.wm = 16; p.ks = 1; p.kd = 32;
   } else {
-    p.nwm = 2; p.wm = 32; p.ks = 4; p.kd = 64;
+    p.nwm = 4; p.wm = 16; p.ks = 2; p.kd = 32;
   }
   p.mt = p.nwm * p.wm;
   p.kin = p.col ? d->Q : d->L;
@@ -591,9 +632,8 @@ void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const Con
 template <bool COL>
 void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                      const ContractParams& prm, cudaStream_t st) {
-  if (p.wm == 16) return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 8>(nt, xm, um, prm, st);
-  if (p.ks == 2) return dispatch_nt<COL, false, 4, 32, 2, 32, 1, 4>(nt, xm, um, prm, st);
-  return dispatch_nt<COL, false, 2, 32, 4, 64, 1, 4>(nt, xm, um, prm, st);
+  if (p.ks == 1) return dispatch_nt<COL, false, 8, 16, 1, 32, 1, 8>(nt, xm, um, prm, st);
+  return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 8>(nt, xm, um, prm, st);
 }
 
 void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
