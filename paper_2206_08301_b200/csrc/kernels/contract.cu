@@ -78,6 +78,67 @@ __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col
 
 // Shared-memory stage: X tile, U tile, and (REDUCE) the stage's Khatri-Rao
 // scale row.  Every piece starts on a 1 KB boundary (SWIZZLE_128B atoms).
+// Incremental Khatri-Rao row: the outer index o is a mixed-radix number over
+// the concatenated factor list (pre..., mid...) — o = p*Q + q for ROW, o = p
+// for COL — and consecutive o differ in the last digit(s) only, so the
+// prefix products are kept and only the factors whose digit changed are
+// re-read (one L1-resident load per column for a step of the last digit).
+struct KrpIter {
+  static constexpr int kMax = 2 * kMaxFac;
+  int n = 0;
+  const double* ptr[kMax];
+  int64_t ext[kMax], ld[kMax], dig[kMax];
+  double pre[kMax + 1][2];  // pre[f] = product of factors 0..f-1, columns c0, c1
+  int c0 = 0, c1 = 0;
+  bool v0 = false, v1 = false;
+
+  __device__ void setup(const FacList& a, const FacList& b, bool use_b, int col0, int col1,
+                        bool ok0, bool ok1) {
+    n = 0;
+    for (int i = 0; i < a.n; ++i, ++n) {
+      ptr[n] = a.ptr[i];
+      ext[n] = a.ext[i];
+      ld[n] = a.ld[i];
+    }
+    if (use_b)
+      for (int i = 0; i < b.n; ++i, ++n) {
+        ptr[n] = b.ptr[i];
+        ext[n] = b.ext[i];
+        ld[n] = b.ld[i];
+      }
+    c0 = col0;
+    c1 = col1;
+    v0 = ok0;
+    v1 = ok1;
+  }
+  __device__ void refresh(int from) {
+    for (int f = from; f < n; ++f) {
+      const double* row = ptr[f] + dig[f] * ld[f];
+      pre[f + 1][0] = v0 ? pre[f][0] * __ldg(row + c0) : 0.0;
+      pre[f + 1][1] = v1 ? pre[f][1] * __ldg(row + c1) : 0.0;
+    }
+  }
+  __device__ void seek(int64_t o) {
+    for (int f = n - 1; f >= 0; --f) {
+      dig[f] = o % ext[f];
+      o /= ext[f];
+    }
+    pre[0][0] = v0 ? 1.0 : 0.0;
+    pre[0][1] = v1 ? 1.0 : 0.0;
+    refresh(0);
+  }
+  __device__ void step() {
+    int f = n - 1;
+    while (f >= 0) {
+      if (++dig[f] < ext[f]) break;
+      dig[f] = 0;
+      --f;
+    }
+    refresh(f < 0 ? 0 : f);
+  }
+  __device__ double value(int h) const { return pre[n][h]; }
+};
+
 template <bool COL, int MT, int NT, int KD>
 struct Tile {
   static constexpr int kXBytes = MT * KD * 8;
@@ -203,6 +264,11 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     uint32_t it = 0;
     int64_t scale_o = -1;
     double sc0 = 0.0, sc1 = 0.0;  // KRP row, columns lane and lane + 32
+    KrpIter krp;
+    if (!BATCHED)
+      krp.setup(prm.pre, prm.mid, !COL, prm.col0 + lane, prm.col0 + lane + 32,
+                lane < NT * 8 && prm.col0 + lane < prm.R,
+                lane + 32 < NT * 8 && prm.col0 + lane + 32 < prm.R);
     Cursor cur;
     cur.seek(i0, BATCHED, prm);
     for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
@@ -210,18 +276,13 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
       const int64_t kc_begin = cur.kc;
       const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
       if (!BATCHED && o != scale_o) {
+        if (scale_o >= 0 && o == scale_o + 1)
+          krp.step();
+        else
+          krp.seek(o);
         scale_o = o;
-        const int64_t p = COL ? o : o / prm.Q;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = lane + 32 * h;
-          double v = 0.0;
-          if (col < NT * 8 && prm.col0 + col < prm.R) {
-            v = krp_value(prm.pre, p, prm.col0 + col);
-            if (!COL) v *= krp_value(prm.mid, o % prm.Q, prm.col0 + col);
-          }
-          (h ? sc1 : sc0) = v;
-        }
+        sc0 = krp.value(0);
+        sc1 = krp.value(1);
       }
       for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
         const int st = it % S;
