@@ -64,9 +64,12 @@ def workload(name: str, P: int):
     def seeded_builder(e, shared_seed=None):
         ins, _ = e.split("->")[0].split(","), None
 
-        def build(pinned):
+        def build(pinned, skip_x=False):
             out = []
             for k, t in enumerate(ins):
+                if k == 0 and skip_x:
+                    out.append(None)
+                    continue
                 shape = tuple(ext[s] for s in t)
                 seed = k if shared_seed is None else (0 if k == 0 else C2_FACTOR_SEED[t[0]])
                 out.append(_fill(shape, seed, pinned and k == 0))
@@ -311,13 +314,24 @@ def main():
         nccl_id = obj[0]
     stream = torch.cuda.Stream()
     execs, inputs, grids, flops_tree = [], [], [], 0
-    for e, ext, build in modes:
-        ins = build(pinned=(world == 1))
+    x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
+    for mi, (e, ext, build) in enumerate(modes):
+        ins = build(pinned=(world == 1)) if mi == 0 else None
         ex = eb.Executor(e, ext, P, 1024.0, rank if world > 1 else -1, nccl_id,
                          stream=stream.cuda_stream)
-        ex.stage(ins)
+        shared = False
+        if mi > 0 and args.config == "C2":
+            # the CP-ALS sweep: one X in HBM for the three modes (eb_exec_share_input)
+            ins = build(pinned=False, skip_x=True)
+            ins[0] = inputs[0][0]
+            ex.share_input(0, execs[0], 0)
+            shared = True
+        elif mi > 0:
+            ins = build(pinned=(world == 1))
+        ex.stage([None] + ins[1:] if shared else ins)
         execs.append(ex)
         inputs.append(ins)
+        x_shared.append(shared)
         plan = json.loads(eb.plan_json(e, ext, P))
         grids.append([t["grid"] for t in plan["schedule"]["terms"]])
         flops_tree += plan["tree"]["total_flops"]
@@ -371,9 +385,9 @@ def main():
     if not args.no_e2e:
         outs = [np.empty(ex_.gather().size) for ex_ in execs]
         h2d = 0
-        for ins, ex_ in zip(inputs, execs):
-            # bytes this rank copies: its blocks of every operand
-            h2d += _staged_bytes(ex_, ins, P, rank if world > 1 else -1, eb)
+        for ins, ex_, sh in zip(inputs, execs, x_shared):
+            # bytes this rank copies: its blocks of every operand it stages
+            h2d += _staged_bytes(ex_, ins, P, rank if world > 1 else -1, eb, skip0=sh)
         d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
         reps = max(1, min(args.steps, 3))
         if world > 1:
@@ -381,8 +395,8 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(reps):
-            for ins, ex_, out in zip(inputs, execs, outs):
-                ex_.stage(ins)
+            for ins, ex_, out, sh in zip(inputs, execs, outs, x_shared):
+                ex_.stage([None] + list(ins[1:]) if sh else ins)
                 ex_.run()
                 ex_.gather(out)
         torch.cuda.synchronize()
@@ -448,7 +462,9 @@ def _x_bytes(modes, P):
     return tot
 
 
-def _staged_bytes(ex, ins, P, rank, eb):
+def _staged_bytes(ex, ins, P, rank, eb, skip0=False):
+    if skip0:
+        ins = [np.empty(0)] + list(ins[1:])
     if P == 1:
         return sum(a.nbytes for a in ins)
     # Blocks of this rank: every operand is split over the grid dims it spans
@@ -458,13 +474,15 @@ def _staged_bytes(ex, ins, P, rank, eb):
         for p in t["placements"]:
             if p["tensor"].startswith("in"):
                 k = int(p["tensor"][2:])
-                tot += ins[k].nbytes // p["owners"]
+                tot += ins[k].nbytes // p["owners"] if ins[k] is not None else 0
     return tot
 
 
 def _ext_of(ex, ins):
     ext = {}
     for t, a in zip(ex.einsum.split("->")[0].split(","), ins):
+        if a is None or a.size == 0:
+            continue
         for c, n in zip(t, a.shape):
             ext[c] = n
     return ext

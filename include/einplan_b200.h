@@ -130,6 +130,11 @@ int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double f
 void eb_exec_destroy(eb_exec* h);
 /* scatter (executor.cpp:48-65): host global inputs -> this process's blocks */
 int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
+/* a NULL entry in host_inputs keeps that operand's device blocks as they are */
+/* alias operand k_dst of `dst` to the staged device blocks of operand k_src of
+ * `src` (same shape and placement on every owned rank, checked); `dst` then
+ * stages NULL for it (e.g. one X shared by the three modes of a CP-ALS sweep) */
+int eb_exec_share_input(eb_exec* dst, int k_dst, eb_exec* src, int k_src);
 /* all terms: local contractions + reductions + redistributions, device only */
 int eb_exec_run(eb_exec* h);
 /* gather canonical output blocks to host (virtual mode, or rank 0) */

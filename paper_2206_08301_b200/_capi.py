@@ -48,7 +48,7 @@ EXPORTS = [
     "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_step_generic",
     "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_destroy", "eb_exec_stage",
-    "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
+    "eb_exec_share_input", "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
     "eb_exec_report_json", "eb_launch_count", "eb_timer_enable", "eb_timer_collect",
 ]
 
@@ -105,6 +105,7 @@ def lib():
         _sig(L, "eb_exec_destroy", None, [_vp])
         _sig(L, "eb_exec_stage", ctypes.c_int, [_vp, ctypes.POINTER(_dp)])
         _sig(L, "eb_exec_run", ctypes.c_int, [_vp])
+        _sig(L, "eb_exec_share_input", ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int])
         _sig(L, "eb_exec_gather", ctypes.c_int, [_vp, _dp])
         _sig(L, "eb_exec_output_elems", _i64, [_vp])
         _sig(L, "eb_exec_stats", ctypes.c_int, [_vp, ctypes.POINTER(_i64)])

@@ -431,6 +431,13 @@ int eb_exec_stage(eb_exec* h, const double* const* host_inputs) {
   });
 }
 
+int eb_exec_share_input(eb_exec* dst, int k_dst, eb_exec* src, int k_src) {
+  return exec_guard([&] {
+    if (!dst || !src) throw eb::InvalidError("eb_exec_share_input: null handle");
+    dst->exec->share_input(k_dst, *src->exec, k_src);
+  });
+}
+
 int eb_exec_run(eb_exec* h) {
   return exec_guard([&] { h->exec->execute(); });
 }

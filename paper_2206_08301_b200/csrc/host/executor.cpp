@@ -303,24 +303,65 @@ void ScheduleExecutor::stage_inputs(const std::vector<const double*>& globals) {
   const auto& spec = pipe_.spec;
   if (globals.size() != spec.inputs.size())
     fail(errc::invalid_argument, "stage: operand count mismatch");
-  input_arena_.release(stream_);
-  inputs_.clear();
+  // Device blocks are allocated on the first stage and reused afterwards, so
+  // that blocks aliased by another executor (share_input) stay valid.  A
+  // null host pointer keeps the operand's current device contents.
   for (const TermPlan& term : pipe_.schedule.terms) {
     for (const AccessArray& arr : term.statement.arrays) {
       if (arr.tensor.rfind("in", 0) != 0) continue;
       const std::size_t k = static_cast<std::size_t>(std::stoi(arr.tensor.substr(2)));
       const TensorPlacement& place = term.placement_of(arr.tensor);
       const auto gshape = spec.shape_of(spec.inputs[k]);
+      const auto key = std::make_pair(term.index, arr.tensor);
+      auto it = inputs_.find(key);
+      if (it == inputs_.end()) {
+        std::vector<DevBlock> blocks(static_cast<std::size_t>(pipe_.schedule.procs));
+        for (std::int64_t r : owned_) {
+          DevBlock& b = blocks[static_cast<std::size_t>(r)];
+          const auto bc = place.block_coords_of(r);
+          b.base = place.dist.base_of(bc);
+          b.shape = place.dist.shape_of(bc);
+          b.ptr = input_arena_.alloc(prod(b.shape), stream_, false);
+        }
+        it = inputs_.emplace(key, std::move(blocks)).first;
+      }
+      if (globals[k] == nullptr) continue;
+      if (aliased_.count(key))
+        fail(errc::invalid_argument, "stage: operand " + arr.tensor +
+                                         " is shared from another executor; pass NULL for it");
+      for (std::int64_t r : owned_) copy_block_h2d(globals[k], gshape, it->second[r]);
+    }
+  }
+  staged_ = true;
+}
+
+void ScheduleExecutor::share_input(int k, const ScheduleExecutor& src, int k_src) {
+  const std::string name = "in" + std::to_string(k), sname = "in" + std::to_string(k_src);
+  if (!src.staged_) fail(errc::invalid_argument, "share_input: source executor not staged");
+  if (pipe_.spec.shape_of(pipe_.spec.inputs[static_cast<std::size_t>(k)]) !=
+      src.pipe_.spec.shape_of(src.pipe_.spec.inputs[static_cast<std::size_t>(k_src)]))
+    fail(errc::invalid_argument, "share_input: operand shapes differ");
+  const std::vector<DevBlock>* from = nullptr;
+  for (const auto& kv : src.inputs_)
+    if (kv.first.second == sname) from = &kv.second;
+  if (!from) fail(errc::invalid_argument, "share_input: source holds no " + sname);
+  for (const TermPlan& term : pipe_.schedule.terms) {
+    for (const AccessArray& arr : term.statement.arrays) {
+      if (arr.tensor != name) continue;
+      const TensorPlacement& place = term.placement_of(name);
       std::vector<DevBlock> blocks(static_cast<std::size_t>(pipe_.schedule.procs));
       for (std::int64_t r : owned_) {
-        DevBlock& b = blocks[static_cast<std::size_t>(r)];
         const auto bc = place.block_coords_of(r);
-        b.base = place.dist.base_of(bc);
-        b.shape = place.dist.shape_of(bc);
-        b.ptr = input_arena_.alloc(prod(b.shape), stream_, false);
-        copy_block_h2d(globals[k], gshape, b);
+        const DevBlock& sb = (*from)[static_cast<std::size_t>(r)];
+        if (sb.base != place.dist.base_of(bc) || sb.shape != place.dist.shape_of(bc))
+          fail(errc::invalid_argument,
+               "share_input: the two schedules place " + name + " differently on rank " +
+                   std::to_string(r));
+        blocks[static_cast<std::size_t>(r)] = sb;
       }
-      inputs_[{term.index, arr.tensor}] = std::move(blocks);
+      const auto key = std::make_pair(term.index, name);
+      inputs_[key] = std::move(blocks);
+      aliased_.insert(key);
     }
   }
 }
@@ -585,7 +626,7 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
 }
 
 void ScheduleExecutor::execute() {
-  if (inputs_.empty()) fail(errc::invalid_argument, "execute: inputs not staged");
+  if (!staged_) fail(errc::invalid_argument, "execute: inputs not staged");
   run_arena_.release(stream_);
   store_.clear();
   comm_ = CommStats{};

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -98,6 +99,10 @@ class ScheduleExecutor {
 
   // scatter (executor.cpp:48-65): every owned rank's input blocks to device.
   void stage_inputs(const std::vector<const double*>& global_inputs);
+  // Use another executor's staged device blocks for operand k (same tensor,
+  // same placement on every owned rank): e.g. one X for the three MTTKRP
+  // modes of a CP-ALS sweep.
+  void share_input(int k, const ScheduleExecutor& src, int k_src);
   // All terms: local contractions, reductions, redistributions (device only).
   void execute();
   // Canonical output blocks to host (virtual, or rank 0 over NCCL).
@@ -132,6 +137,8 @@ class ScheduleExecutor {
   std::vector<std::int64_t> owned_;
   std::map<std::pair<int, std::string>, std::vector<DevBlock>> inputs_;
   std::map<std::pair<int, std::string>, std::vector<DevBlock>> store_;
+  std::set<std::pair<int, std::string>> aliased_;
+  bool staged_ = false;
   DeviceArena input_arena_, run_arena_;
   void* workspace_ = nullptr;
   std::size_t workspace_bytes_ = 0;

@@ -477,13 +477,32 @@ __global__ void reduce_partials_kernel(const double* __restrict__ ws, double* __
   //   c >= ceil((lo+1)*G/items) - 1  and  c <= ceil(hi*G/items) - 1.
   const int64_t cmin = ((lo + 1) * G + items - 1) / items - 1;
   const int64_t cmax = (hi * G + items - 1) / items - 1;
+  // Gather the contributions in batches of independent loads (the partial
+  // slots are read once; a serial load->add chain would be latency-bound),
+  // then add them in ascending (CTA, k-split) order.
+  constexpr int kBatch = 16;
   double acc = 0.0;
-  for (int64_t c = cmin < 0 ? 0 : cmin; c <= cmax && c < G; ++c) {
-    const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
-    if (c1 <= lo || c0 >= hi || c1 <= c0) continue;
-    const int64_t sg = t - c0 / per_tile;
-    for (int k = 0; k < KS; ++k)
-      acc += ws[(((c * segmax + sg) * KS + k) * MT + (m % MT)) * NP + n];
+  const int64_t cbeg = cmin < 0 ? 0 : cmin;
+  const int64_t cend = (cmax < G - 1 ? cmax : G - 1) + 1;
+  const int64_t total = (cend - cbeg) * KS;
+  for (int64_t b = 0; b < total; b += kBatch) {
+    double v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      v[u] = 0.0;
+      const int64_t e = b + u;
+      if (e < total) {
+        const int64_t c = cbeg + e / KS;
+        const int k = (int)(e % KS);
+        const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
+        if (!(c1 <= lo || c0 >= hi || c1 <= c0)) {
+          const int64_t sg = t - c0 / per_tile;
+          v[u] = ws[(((c * segmax + sg) * KS + k) * MT + (m % MT)) * NP + n];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) acc += v[u];
   }
   out[m * ldo + col0 + n] = acc;
 }

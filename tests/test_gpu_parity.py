@@ -286,3 +286,30 @@ def test_reference_c_smoke_runs_on_gpu(eb):
         pytest.skip("capi_smoke not built (needs the reference sources at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
+
+
+def test_share_input_across_modes(eb):
+    """One X staged once and aliased by the three MTTKRP executors of a sweep
+    (eb_exec_share_input); each mode must still match the oracle."""
+    ext = dict(i=48, j=40, k=36, a=16)
+    es = ["ijk,ja,ka->ia", "ijk,ia,ka->ja", "ijk,ia,ja->ka"]
+    X = oracle.random_tensor((48, 40, 36), 0)
+    F = {c: oracle.random_tensor((ext[c], 16), s) for c, s in (("i", 1), ("j", 2), ("k", 3))}
+    ex0 = None
+    for m, e in enumerate(es):
+        ins, _ = oracle.parse(e)
+        ops = [X] + [F[t[0]] for t in ins[1:]]
+        for P in (1, 4):
+            ex = eb.Executor(e, ext, P)
+            if m == 0:
+                ex.stage(ops)
+                if P == 4:
+                    ex0 = ex
+            else:
+                if P == 4:
+                    ex.share_input(0, ex0, 0)
+                    ex.stage([None] + ops[1:])
+                else:
+                    ex.stage(ops)
+            ex.run()
+            check(ex.gather(), oracle.naive_evaluate(e, ext, ops))
