@@ -78,72 +78,47 @@ __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col
 
 // Shared-memory stage: X tile, U tile, and (REDUCE) the stage's Khatri-Rao
 // scale row.  Every piece starts on a 1 KB boundary (SWIZZLE_128B atoms).
-// Incremental Khatri-Rao row: the outer index o is a mixed-radix number over
-// the concatenated factor list (pre..., mid...) — o = p*Q + q for ROW, o = p
-// for COL — and consecutive o differ in the last digit(s) only, so the
-// prefix products are kept and only the factors whose digit changed are
-// re-read (one L1-resident load per column for a step of the last digit).
-struct KrpIter {
-  static constexpr int kMax = 2 * kMaxFac;
-  int n = 0;
-  const double* ptr[kMax];
-  int64_t ext[kMax], ld[kMax], dig[kMax];
-  double pre[kMax + 1][2];  // pre[f] = product of factors 0..f-1, columns c0, c1
-  int c0 = 0, c1 = 0;
-  bool v0 = false, v1 = false;
-
-  __device__ void setup(const FacList& a, const FacList& b, bool use_b, int col0, int col1,
-                        bool ok0, bool ok1) {
-    n = 0;
-    for (int i = 0; i < a.n; ++i, ++n) {
-      ptr[n] = a.ptr[i];
-      ext[n] = a.ext[i];
-      ld[n] = a.ld[i];
-    }
-    if (use_b)
-      for (int i = 0; i < b.n; ++i, ++n) {
-        ptr[n] = b.ptr[i];
-        ext[n] = b.ext[i];
-        ld[n] = b.ld[i];
-      }
-    c0 = col0;
-    c1 = col1;
-    v0 = ok0;
-    v1 = ok1;
-  }
-  __device__ void refresh(int from) {
-    for (int f = from; f < n; ++f) {
-      const double* row = ptr[f] + dig[f] * ld[f];
-      pre[f + 1][0] = v0 ? pre[f][0] * __ldg(row + c0) : 0.0;
-      pre[f + 1][1] = v1 ? pre[f][1] * __ldg(row + c1) : 0.0;
-    }
-  }
-  __device__ void seek(int64_t o) {
-    for (int f = n - 1; f >= 0; --f) {
-      dig[f] = o % ext[f];
-      o /= ext[f];
-    }
-    pre[0][0] = v0 ? 1.0 : 0.0;
-    pre[0][1] = v1 ? 1.0 : 0.0;
-    refresh(0);
-  }
-  __device__ void step() {
-    int f = n - 1;
-    while (f >= 0) {
-      if (++dig[f] < ext[f]) break;
-      dig[f] = 0;
-      --f;
-    }
-    refresh(f < 0 ? 0 : f);
-  }
-  __device__ double value(int h) const { return pre[n][h]; }
+// Khatri-Rao value cache of one producer lane.  The outer index o is a
+// mixed-radix number over the concatenated factor list (pre..., mid...):
+// o = p*Q + q (ROW) or o = p (COL).  Value slot u of the lane is a fixed
+// (stage-relative outer index, column); consecutive stage groups move it by
+// OS outer indices, which changes the last digit only (one L1-resident factor
+// load) except on a carry, when the prefix product over the other factors is
+// recomputed.  No division on the steady-state path.
+struct KrpSlot {
+  int64_t digit = -1;  // last-factor digit of the slot's current outer index
+  int64_t rest = -1;   // o / e_last
+  double prefix = 0.0; // product of the other factors' rows at `rest`
 };
 
-template <bool COL, int MT, int NT, int KD>
+__device__ __forceinline__ const FacList& krp_last_list(const ContractParams& p, bool col) {
+  return (!col && p.mid.n > 0) ? p.mid : p.pre;
+}
+
+__device__ double krp_prefix(const ContractParams& prm, bool col, int64_t rest, int c) {
+  // all factors but the last, mixed radix (mid digits least significant)
+  double v = 1.0;
+  const bool last_in_mid = !col && prm.mid.n > 0;
+  if (!col) {
+    for (int f = prm.mid.n - 1 - (last_in_mid ? 1 : 0); f >= 0; --f) {
+      const int64_t e = prm.mid.ext[f];
+      v *= __ldg(prm.mid.ptr[f] + (rest % e) * prm.mid.ld[f] + c);
+      rest /= e;
+    }
+  }
+  for (int f = prm.pre.n - 1 - (last_in_mid ? 0 : 1); f >= 0; --f) {
+    const int64_t e = prm.pre.ext[f];
+    v *= __ldg(prm.pre.ptr[f] + (rest % e) * prm.pre.ld[f] + c);
+    rest /= e;
+  }
+  return v;
+}
+
+template <bool COL, int MT, int NT, int KD, int OS>
 struct Tile {
-  static constexpr int kXBytes = MT * KD * 8;
+  static constexpr int kXBytes = MT * KD * 8 * OS;
   static constexpr int kUBytes = COL ? ((NT * 8 + 15) / 16) * KD * 128 : NT * 8 * KD * 8;
-  static constexpr int kScaleBytes = 1024;  // NT*8 <= 64 doubles
+  static constexpr int kScaleBytes = ((OS * NT * 64) + 1023) / 1024 * 1024;  // OS KRP rows
   static constexpr int kStageBytes = kXBytes + kUBytes + kScaleBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024;
@@ -192,11 +167,11 @@ __device__ __forceinline__ void fold_krp(double (&t)[MI][NT][2], double (&m)[MI]
 
 // Store one row tile's register accumulators into partial slot (sg, ks) of
 // this CTA and clear them.
-template <int MI, int NT, int MT, int WM, int KS>
+template <int MI, int NT, int MT, int WM, int SPL>
 __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const ContractParams& prm,
-                                              int sg, int wm, int ks, int g, int l) {
+                                              int sg, int wm, int split, int g, int l) {
   double* dst = prm.out +
-                (((int64_t)blockIdx.x * prm.segmax + sg) * KS + ks) * (int64_t)MT * (NT * 8);
+                (((int64_t)blockIdx.x * prm.segmax + sg) * SPL + split) * (int64_t)MT * (NT * 8);
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -212,23 +187,28 @@ __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const Co
 //   warp NCW       producer: lane 0 fills the stage ring with TMA boxes of X
 //                  and U; all 32 lanes write the stage's Khatri-Rao row
 //                  KRP(pre)[p] * KRP(mid)[q] (REDUCE) next to it.
-//   warps 0..NCW-1 consumers: warp w owns rows (w % NWM)*WM.. of the CTA tile
-//                  and the 16-deep k groups g16 of each stage with
-//                  g16 % KS == w / NWM.
+//   warps 0..NCW-1 consumers: warp w owns rows (w % NWM)*WM.. of the CTA tile,
+//                  the 16-deep k groups g16 of each stage with
+//                  g16 % KS == (w / NWM) % KS, and outer index o_base + w / (NWM*KS)
+//                  of the stage's OS consecutive outer indices (a stage holds
+//                  OS x MT x KD of X: long contiguous runs per X row when the
+//                  output has few rows, e.g. order-5 mode 0).
 // REDUCE (MTTKRP) accumulates in two levels: T = sum over the k chunks of one
 // outer index o of X·U on DMMA (B fragments straight from shared memory),
 // then M += KRP[o] (.) T once per outer index — the Khatri-Rao product is a
 // per-column scale of T and is never formed.  One partial per k-split group.
 // BATCHED (TTM) requires KS == 1 and writes each (row tile, o) unit once.
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT>
-__global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT>
+__global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
   static_assert(KD % (16 * KS) == 0, "each k-split group owns whole 16-deep groups");
+  static_assert(!BATCHED || OS == 1, "BATCHED stages one outer index");
   constexpr int MT = NWM * WM;
   constexpr int MI = WM / 8;  // m8 tiles per warp
-  constexpr int NCW = NWM * KS;
-  using T = Tile<COL, MT, NT, KD>;
+  constexpr int NCW = NWM * KS * OS;
+  constexpr int SPL = KS * OS;  // partial slots per row tile
+  using T = Tile<COL, MT, NT, KD, OS>;
   constexpr int S = T::kStages;
   static_assert(!BATCHED || KS == 1, "BATCHED writes each unit once");
 
@@ -245,7 +225,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_addr(&full_bar[s]), 1);
+      mbar_init(smem_addr(&full_bar[s]), BATCHED ? 1 : 2);  // TMA tx (+ KRP row)
       mbar_init(smem_addr(&empty_bar[s]), NCW);
     }
     mbar_fence_init();
@@ -262,59 +242,95 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
       tma_prefetch_desc(&umap);
     }
     uint32_t it = 0;
-    int64_t scale_o = -1;
-    double sc0 = 0.0, sc1 = 0.0;  // KRP row, columns lane and lane + 32
-    KrpIter krp;
-    if (!BATCHED)
-      krp.setup(prm.pre, prm.mid, !COL, prm.col0 + lane, prm.col0 + lane + 32,
-                lane < NT * 8 && prm.col0 + lane < prm.R,
-                lane + 32 < NT * 8 && prm.col0 + lane + 32 < prm.R);
+    int64_t scale_g = -1;  // outer-index group whose KRP rows are in kv[]
+    // The stage's OS x NP Khatri-Rao values, spread over the 32 lanes: slot
+    // u holds value v = lane + 32u = (outer index v / NP, column v % NP).
+    constexpr int NP = NT * 8;
+    constexpr int VPL = (OS * NP + 31) / 32;
+    double kv[VPL];
+    KrpSlot slot[VPL];
+    const bool has_krp = (COL ? 0 : prm.mid.n) + prm.pre.n > 0;
     Cursor cur;
     cur.seek(i0, BATCHED, prm);
     for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
       const int64_t mt = cur.mt, o = cur.o;
       const int64_t kc_begin = cur.kc;
       const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
-      if (!BATCHED && o != scale_o) {
-        if (scale_o >= 0 && o == scale_o + 1)
-          krp.step();
-        else
-          krp.seek(o);
-        scale_o = o;
-        sc0 = krp.value(0);
-        sc1 = krp.value(1);
-      }
       for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
         const int st = it % S;
         if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
-        if (!BATCHED) {
-          double* sc = reinterpret_cast<double*>(sbase + st * T::kStageBytes + T::kXBytes +
-                                                 T::kUBytes);
-          if (lane < NT * 8) sc[lane] = sc0;
-          if (lane + 32 < NT * 8) sc[lane + 32] = sc1;
-          __syncwarp();
-        }
+        const uint32_t fb = smem_addr(&full_bar[st]);
         if (lane == 0) {
-          const uint32_t fb = smem_addr(&full_bar[st]);
+          // TMA first: the KRP row below is computed while the boxes fly.
           mbar_expect_tx(fb, T::kXBytes + T::kUBytes);
           const uint32_t xs = base + st * T::kStageBytes;
           const uint32_t us = xs + T::kXBytes;
           const int k0 = (int)(kc * KD);
+          const int64_t ob = o * OS;  // first outer index of the stage
           if (!COL) {
-            const int p = (int)(o / prm.Q), q = (int)(o % prm.Q);
+            // X map dims {L, M, Q, P}: box {16, MT, OS, 1} -> smem [OS][MT][16]
+            const int p = (int)(ob / prm.Q), q = (int)(ob % prm.Q);
 #pragma unroll
             for (int b = 0; b < KD / 16; ++b) {
-              tma_load_4d(xs + b * MT * 128, &xmap, fb, k0 + 16 * b, q, (int)(mt * MT), p);
+              tma_load_4d(xs + b * OS * MT * 128, &xmap, fb, k0 + 16 * b, (int)(mt * MT), q, p);
               tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, 0);
             }
           } else {
+            // X map dims {M, Q, P}: box {16, KD, OS} -> smem [OS][KD][16]
 #pragma unroll
             for (int b = 0; b < MT / 16; ++b)
-              tma_load_3d(xs + b * KD * 128, &xmap, fb, (int)(mt * MT) + 16 * b, k0, (int)o);
+              tma_load_3d(xs + b * OS * KD * 128, &xmap, fb, (int)(mt * MT) + 16 * b, k0, (int)ob);
 #pragma unroll
             for (int b = 0; b < (NT * 8 + 15) / 16; ++b)
               tma_load_2d(us + b * KD * 128, &umap, fb, prm.col0 + 16 * b, k0);
           }
+        }
+        if (!BATCHED) {
+          if (o != scale_g) {
+            const bool next = scale_g >= 0 && o == scale_g + 1;
+            scale_g = o;
+            const FacList& lastl = krp_last_list(prm, COL);
+            const int nl = lastl.n;
+#pragma unroll
+            for (int u = 0; u < VPL; ++u) {
+              const int v = lane + 32 * u;
+              const int col = v % NP;
+              double val = 0.0;
+              if (v < OS * NP && prm.col0 + col < prm.R) {
+                const int c = prm.col0 + col;
+                if (!has_krp) {
+                  val = 1.0;
+                } else {
+                  const int64_t e = lastl.ext[nl - 1];
+                  KrpSlot& sl = slot[u];
+                  if (next && sl.digit >= 0) {
+                    sl.digit += OS;
+                    bool carry = false;
+                    while (sl.digit >= e) {
+                      sl.digit -= e;
+                      ++sl.rest;
+                      carry = true;
+                    }
+                    if (carry) sl.prefix = krp_prefix(prm, COL, sl.rest, c);
+                  } else {
+                    const int64_t oo = o * OS + v / NP;
+                    sl.digit = oo % e;
+                    sl.rest = oo / e;
+                    sl.prefix = krp_prefix(prm, COL, sl.rest, c);
+                  }
+                  val = sl.prefix * __ldg(lastl.ptr[nl - 1] + sl.digit * lastl.ld[nl - 1] + c);
+                }
+              }
+              kv[u] = val;
+            }
+          }
+          double* sc = reinterpret_cast<double*>(sbase + st * T::kStageBytes + T::kXBytes +
+                                                 T::kUBytes);
+#pragma unroll
+          for (int u = 0; u < VPL; ++u)
+            if (lane + 32 * u < OS * NP) sc[lane + 32 * u] = kv[u];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(fb);  // second arrival: the KRP row is in place
         }
       }
     }
@@ -322,7 +338,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
   }
 
   // -------------------------------------------------------------- consumers
-  const int wm = warp % NWM, ks = warp / NWM;
+  const int wm = warp % NWM, ks = (warp / NWM) % KS, os = warp / (NWM * KS);
   const int g = lane >> 2, l = lane & 3;
   double acc[MI][NT][2];                 // T: this outer index (or the TTM unit)
   double macc[BATCHED ? 1 : MI][NT][2];  // M: the row tile's MTTKRP partial
@@ -373,7 +389,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
     if constexpr (!BATCHED) if (o != cur_o || mt != cur_mt) {
       if (cur_o >= 0) fold_krp<MI, NT>(acc, macc, krow);
       if (mt != cur_mt) {
-        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, KS>(macc, prm, seg, wm, ks, g, l);
+        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
         ++seg;
         cur_mt = mt;
       }
@@ -385,8 +401,8 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
                                                          T::kXBytes + T::kUBytes);
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        krow[j][0] = sc[j * 8 + 2 * l];
-        krow[j][1] = sc[j * 8 + 2 * l + 1];
+        krow[j][0] = sc[os * NT * 8 + j * 8 + 2 * l];
+        krow[j][1] = sc[os * NT * 8 + j * 8 + 2 * l + 1];
       }
     }
     for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
@@ -404,9 +420,9 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
           const int m8 = wm * MI + i;  // m8 tile index inside the CTA tile
           uint32_t o_a;
           if (!COL)
-            o_a = b16 * MT * 128 + m8 * 8 * 128 + off[s][0];
+            o_a = (b16 * OS + os) * MT * 128 + m8 * 8 * 128 + off[s][0];
           else
-            o_a = (m8 >> 1) * KD * 128 + b16 * 16 * 128 + off[s][m8 & 1];
+            o_a = ((m8 >> 1) * OS + os) * KD * 128 + b16 * 16 * 128 + off[s][m8 & 1];
           a[i] = *reinterpret_cast<const double*>(xs + o_a);
         }
 #pragma unroll
@@ -455,7 +471,7 @@ __global__ void __launch_bounds__((NWM * KS + 1) * 32, 1)
   if constexpr (!BATCHED) {
     if (cur_mt >= 0) {
       fold_krp<MI, NT>(acc, macc, krow);
-      flush_partial<MI, NT, MT, WM, KS>(macc, prm, seg, wm, ks, g, l);
+      flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
     }
   }
 }
@@ -606,7 +622,7 @@ FacList to_list(int n, const eb_factor* f) {
 
 struct Plan {
   bool col = false, batched = false;
-  int nwm = 4, wm = 32, ks = 2, kd = 32, nt = 4;
+  int nwm = 4, wm = 32, ks = 2, kd = 32, os = 1, nt = 4;
   int mt = 128;
   int64_t kin = 0, O = 0, KC = 0, mtiles = 0, items = 0;
   int G = 0, segmax = 0;
@@ -639,18 +655,23 @@ Plan plan_of(const eb_contract_desc* d) {
   // Tile configurations (instantiated in dispatch below):
   //   REDUCE, M >= 128 : 8 row warps x 16 rows, 32-deep stages
   //   REDUCE, M <  128 : 4 row warps x 16 rows, k split 2, 32-deep stages
+  //   REDUCE, M <  128, outer % 4 == 0 : 16-row tiles x 4 outer indices per
+  //                      stage x k split 2, 64-deep (long contiguous X runs)
   //   (two accumulator sets T and M per warp; 9 warps leave 168 registers)
   //   BATCHED          : 4 row warps x 32 (M >= 128) or 16 rows, 32-deep
+  const int64_t outer = p.col ? d->P : d->P * d->Q;
   if (p.batched) {
     p.nwm = 4; p.wm = rows >= 128 ? 32 : 16; p.ks = 1; p.kd = 32;
   } else if (rows >= 128) {
     p.nwm = 8; p.wm = 16; p.ks = 1; p.kd = 32;
+  } else if (outer % 4 == 0 && (p.col || d->Q % 4 == 0)) {
+    p.nwm = 1; p.wm = 16; p.ks = 2; p.kd = 64; p.os = 4;
   } else {
     p.nwm = 4; p.wm = 16; p.ks = 2; p.kd = 32;
   }
   p.mt = p.nwm * p.wm;
   p.kin = p.col ? d->Q : d->L;
-  p.O = p.col ? d->P : d->P * d->Q;
+  p.O = (p.col ? d->P : d->P * d->Q) / p.os;  // outer-index groups
   p.KC = cdiv(p.kin, p.kd);
   p.mtiles = cdiv(rows, p.mt);
   const int sms = sm_count();
@@ -667,7 +688,7 @@ Plan plan_of(const eb_contract_desc* d) {
       if (c1 > c0) segmax = std::max<int>(segmax, (int)((c1 - 1) / per_tile - c0 / per_tile + 1));
     }
     p.segmax = segmax;
-    p.ws_bytes = (size_t)p.G * segmax * p.ks * p.mt * (p.nt * 8) * sizeof(double);
+    p.ws_bytes = (size_t)p.G * segmax * p.ks * p.os * p.mt * (p.nt * 8) * sizeof(double);
   }
   if (p.col) {
     p.u_bytes = (size_t)d->Q * ((d->R + 1) / 2 * 2) * sizeof(double);
@@ -679,18 +700,18 @@ Plan plan_of(const eb_contract_desc* d) {
   return p;
 }
 
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
-  using T = Tile<COL, NWM * WM, NT, KD>;
-  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, NT>;
+  using T = Tile<COL, NWM * WM, NT, KD, OS>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT>;
   static bool attr = false;
   if (!attr) {
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
     attr = true;
   }
   main_kernel_begin(st);
-  kern<<<prm.G, (NWM * KS + 1) * 32, T::kSmem, st>>>(xm, um, prm);
+  kern<<<prm.G, (NWM * KS * OS + 1) * 32, T::kSmem, st>>>(xm, um, prm);
   EB_CUDA(cudaGetLastError());
   main_kernel_end(st);
   count_launch();
@@ -698,12 +719,12 @@ void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams
 
 // Column-tile count dispatch over [NT_LO, NT_HI] (configurations whose
 // accumulators would not fit are never instantiated).
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int NT_LO, int NT_HI>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT_LO, int NT_HI>
 void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
                  cudaStream_t st) {
   if constexpr (NT_LO <= NT_HI) {
-    if (nt == NT_LO) return launch_t<COL, BATCHED, NWM, WM, KS, KD, NT_LO>(xm, um, prm, st);
-    return dispatch_nt<COL, BATCHED, NWM, WM, KS, KD, NT_LO + 1, NT_HI>(nt, xm, um, prm, st);
+    if (nt == NT_LO) return launch_t<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO>(xm, um, prm, st);
+    return dispatch_nt<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO + 1, NT_HI>(nt, xm, um, prm, st);
   } else {
     throw InvalidError("eb_contract: unsupported column tile count");
   }
@@ -712,15 +733,16 @@ void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const Con
 template <bool COL>
 void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                      const ContractParams& prm, cudaStream_t st) {
-  if (p.ks == 1) return dispatch_nt<COL, false, 8, 16, 1, 32, 1, 8>(nt, xm, um, prm, st);
-  return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 8>(nt, xm, um, prm, st);
+  if (p.ks == 1) return dispatch_nt<COL, false, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
+  if (p.os == 4) return dispatch_nt<COL, false, 1, 16, 2, 64, 4, 1, 8>(nt, xm, um, prm, st);
+  return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 1, 8>(nt, xm, um, prm, st);
 }
 
 void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                     const ContractParams& prm, cudaStream_t st) {
   if (p.batched) {
-    if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 8>(nt, xm, um, prm, st);
-    return dispatch_nt<true, true, 4, 16, 1, 32, 1, 8>(nt, xm, um, prm, st);
+    if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
+    return dispatch_nt<true, true, 4, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
   }
   if (p.col) return dispatch_reduce<true>(p, nt, xm, um, prm, st);
   return dispatch_reduce<false>(p, nt, xm, um, prm, st);
@@ -766,15 +788,16 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   }
   CUtensorMap xmap;
   if (!p.col) {
-    const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->Q, (uint64_t)d->M, (uint64_t)d->P};
-    const uint64_t str[3] = {(uint64_t)d->L * 8, (uint64_t)(d->Q * d->L) * 8,
+    // dims {L, M, Q, P} (M before Q so one box holds OS outer indices of MT rows)
+    const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->M, (uint64_t)d->Q, (uint64_t)d->P};
+    const uint64_t str[3] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8,
                              (uint64_t)(d->M * d->Q * d->L) * 8};
-    const uint32_t box[4] = {16, 1, (uint32_t)p.mt, 1};
+    const uint32_t box[4] = {16, (uint32_t)p.mt, (uint32_t)p.os, 1};
     xmap = make_map(d->X, 4, dims, str, box);
   } else {
     const uint64_t dims[3] = {(uint64_t)d->M, (uint64_t)d->Q, (uint64_t)d->P};
     const uint64_t str[2] = {(uint64_t)d->M * 8, (uint64_t)(d->Q * d->M) * 8};
-    const uint32_t box[3] = {16, (uint32_t)p.kd, 1};
+    const uint32_t box[3] = {16, (uint32_t)p.kd, (uint32_t)p.os};
     xmap = make_map(d->X, 3, dims, str, box);
   }
 
@@ -806,7 +829,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
       const int np = nt * 8;
       const int64_t n = d->M * np;
       reduce_partials_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(
-          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks, p.O * p.KC, p.items, p.G,
+          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks * p.os, p.O * p.KC, p.items, p.G,
           p.segmax);
       EB_CUDA(cudaGetLastError());
       count_launch();
