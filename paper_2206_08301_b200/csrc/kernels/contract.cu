@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -120,7 +121,7 @@ struct Tile {
   static constexpr int kUBytes = COL ? ((NT * 8 + 15) / 16) * KD * 128 : NT * 8 * KD * 8;
   static constexpr int kScaleBytes = ((OS * NT * 64) + 1023) / 1024 * 1024;  // OS KRP rows
   static constexpr int kStageBytes = kXBytes + kUBytes + kScaleBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static_assert(kXBytes % 1024 == 0 && kUBytes % 1024 == 0, "swizzle atoms need 1 KB alignment");
   static_assert(kStages >= 2, "stage too large");
@@ -655,8 +656,9 @@ Plan plan_of(const eb_contract_desc* d) {
   // Tile configurations (instantiated in dispatch below):
   //   REDUCE, M >= 128 : 8 row warps x 16 rows, 32-deep stages
   //   REDUCE, M <  128 : 4 row warps x 16 rows, k split 2, 32-deep stages
-  //   REDUCE, M <  128, outer % 4 == 0 : 16-row tiles x 4 outer indices per
-  //                      stage x k split 2, 64-deep (long contiguous X runs)
+  //   REDUCE, M <  128, outer even : 64-row tiles x 2 outer indices per
+  //                      stage, 64-deep (every warp its own (rows, outer index);
+  //                      measured best of 12 tilings for order-5 mode 0)
   //   (two accumulator sets T and M per warp; 9 warps leave 168 registers)
   //   BATCHED          : 4 row warps x 32 (M >= 128) or 16 rows, 32-deep
   const int64_t outer = p.col ? d->P : d->P * d->Q;
@@ -664,8 +666,8 @@ Plan plan_of(const eb_contract_desc* d) {
     p.nwm = 4; p.wm = rows >= 128 ? 32 : 16; p.ks = 1; p.kd = 32;
   } else if (rows >= 128) {
     p.nwm = 8; p.wm = 16; p.ks = 1; p.kd = 32;
-  } else if (outer % 4 == 0 && (p.col || d->Q % 4 == 0)) {
-    p.nwm = 1; p.wm = 16; p.ks = 2; p.kd = 64; p.os = 4;
+  } else if (outer % 2 == 0 && (p.col || d->Q % 2 == 0)) {
+    p.nwm = 4; p.wm = 16; p.ks = 1; p.kd = 64; p.os = 2;
   } else {
     p.nwm = 4; p.wm = 16; p.ks = 2; p.kd = 32;
   }
@@ -733,8 +735,8 @@ void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const Con
 template <bool COL>
 void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                      const ContractParams& prm, cudaStream_t st) {
+  if (p.os == 2) return dispatch_nt<COL, false, 4, 16, 1, 64, 2, 1, 8>(nt, xm, um, prm, st);
   if (p.ks == 1) return dispatch_nt<COL, false, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
-  if (p.os == 4) return dispatch_nt<COL, false, 1, 16, 2, 64, 4, 1, 8>(nt, xm, um, prm, st);
   return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 1, 8>(nt, xm, um, prm, st);
 }
 
