@@ -78,7 +78,7 @@ def workload(name: str, P: int):
 
     modes = []
     for e in c["einsums"]:
-        modes.append((e, ext, seeded_builder(e, shared_seed=(name == "C2"))))
+        modes.append((e, ext, seeded_builder(e, shared_seed=(True if name == "C2" else None))))
     label = {
         "C1": "C1: order-3 MTTKRP mode-0, X 512^3, R=24",
         "C2": "C2: order-3 CP-ALS MTTKRP sweep (modes 0,1,2), X 1024^3 fp64, factors 1024x32",
@@ -357,8 +357,11 @@ def main():
     x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
     for mi, (e, ext, build) in enumerate(modes):
         ins = build(pinned=(world == 1)) if mi == 0 else None
-        ex = eb.Executor(e, ext, P, 1024.0, rank if world > 1 else -1, nccl_id,
-                         stream=stream.cuda_stream)
+        if mi == 0:
+            ex = eb.Executor(e, ext, P, 1024.0, rank if world > 1 else -1, nccl_id,
+                             stream=stream.cuda_stream)
+        else:  # same ranks / same NCCL communicator as mode 0
+            ex = eb.Executor(e, ext, stream=stream.cuda_stream, like=execs[0])
         shared = False
         if mi > 0 and args.config == "C2":
             # the CP-ALS sweep: one X in HBM for the three modes (eb_exec_share_input)
@@ -455,9 +458,14 @@ def main():
         return 0
 
     # Roofline of the dominant kernel (the fused contraction), live events.
+    # All launches of the fused contraction kernel in the timed steps (one per
+    # MTTKRP mode for C1-C3, one per TTM step for C4/C5): algorithmic flops of
+    # the work they do (the reference tree's flops, this rank's 1/P share)
+    # over their CUDA-event time.
     kern_ms = kms.value / max(kn.value, 1)
-    per_launch_flops = flops_tree / len(execs) / P
-    achieved = per_launch_flops / (kern_ms * 1e-3) / 1e12
+    launches_per_step = max(kn.value // max(args.steps, 1), 1)
+    per_launch_flops = flops_tree / P / launches_per_step
+    achieved = (flops_tree / P) / (kms.value / args.steps * 1e-3) / 1e12
     peaks = _load_peaks()
     traffic = _traffic(args.config)
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -467,9 +475,10 @@ def main():
                            "(MEASURED_PEAKS.json has no FP64 figure)",
             "kernel_ms_per_launch": kern_ms, "kernel_launches_timed": kn.value,
             "kernel_share_of_step": kms.value / max(ms, 1e-9),
-            "hbm_achieved_gbs": _x_bytes(modes, P) / len(execs) / (kern_ms * 1e-3) / 1e9,
+            "hbm_achieved_gbs": _x_bytes(modes, P) / (kms.value / args.steps * 1e-3) / 1e9,
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
-            "algorithmic_flops_per_launch": per_launch_flops}
+            "algorithmic_flops_per_launch": per_launch_flops,
+            "launches_per_step": launches_per_step}
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

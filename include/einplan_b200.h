@@ -127,6 +127,11 @@ typedef struct eb_exec eb_exec;
 int eb_nccl_unique_id(void* out128);
 int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double fast_mem,
                    int64_t rank, const void* nccl_id, void* stream, eb_exec** out);
+/* a second executor over the same ranks and the same communicator as `peer`
+ * (an ncclUniqueId initialises exactly one communicator): e.g. the three
+ * MTTKRP modes of a sweep on one process group */
+int eb_exec_create_like(const char* einsum, const char* dims, double fast_mem, eb_exec* peer,
+                        void* stream, eb_exec** out);
 void eb_exec_destroy(eb_exec* h);
 /* scatter (executor.cpp:48-65): host global inputs -> this process's blocks */
 int eb_exec_stage(eb_exec* h, const double* const* host_inputs);

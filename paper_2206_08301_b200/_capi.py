@@ -47,7 +47,7 @@ EXPORTS = [
     "einplan_plan_json", "einplan_run_json", "einplan_bench_json",
     "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_step_generic",
     "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
-    "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_destroy", "eb_exec_stage",
+    "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
     "eb_exec_report_json", "eb_launch_count", "eb_timer_enable", "eb_timer_collect",
 ]
@@ -103,6 +103,8 @@ def lib():
         _sig(L, "eb_exec_create", ctypes.c_int,
              [c, c, _i64, ctypes.c_double, _i64, _vp, _vp, ctypes.POINTER(_vp)])
         _sig(L, "eb_exec_destroy", None, [_vp])
+        _sig(L, "eb_exec_create_like", ctypes.c_int,
+             [c, c, ctypes.c_double, _vp, _vp, ctypes.POINTER(_vp)])
         _sig(L, "eb_exec_stage", ctypes.c_int, [_vp, ctypes.POINTER(_dp)])
         _sig(L, "eb_exec_run", ctypes.c_int, [_vp])
         _sig(L, "eb_exec_share_input", ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int])

@@ -335,7 +335,8 @@ einplan_status einplan_bench_json(double scale, int64_t procs, double fast_mem, 
 // ===================================================== inner eb_exec ABI --
 
 struct eb_exec {
-  std::unique_ptr<gpu::Transport> transport;
+  std::shared_ptr<gpu::Transport> transport;  // shared by executors of one process group
+  int64_t procs = 1;
   std::unique_ptr<gpu::ScheduleExecutor> exec;
   cudaStream_t stream = nullptr;
   double fast_mem = 1024.0;
@@ -406,15 +407,33 @@ int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double f
     h->stream = static_cast<cudaStream_t>(stream);
     Pipeline pipe = make_pipeline(make_spec(einsum, dims), procs, fast_mem);
     if (rank < 0) {
-      h->transport = std::make_unique<gpu::VirtualTransport>(procs);
+      h->transport = std::make_shared<gpu::VirtualTransport>(procs);
     } else {
 #ifdef EB_HAVE_NCCL
       if (!nccl_id) throw eb::InvalidError("eb_exec_create: rank >= 0 needs an NCCL unique id");
-      h->transport = std::make_unique<gpu::NcclTransport>(nccl_id, procs, rank);
+      h->transport = std::make_shared<gpu::NcclTransport>(nccl_id, procs, rank);
 #else
       throw eb::DeviceError("built without NCCL");
 #endif
     }
+    h->procs = procs;
+    h->exec = std::make_unique<gpu::ScheduleExecutor>(std::move(pipe), h->transport.get(),
+                                                      h->stream);
+    *out = h.release();
+  });
+}
+
+int eb_exec_create_like(const char* einsum, const char* dims, double fast_mem, eb_exec* peer,
+                        void* stream, eb_exec** out) {
+  return exec_guard([&] {
+    if (!out || !peer) throw eb::InvalidError("eb_exec_create_like: null argument");
+    *out = nullptr;
+    auto h = std::make_unique<eb_exec>();
+    h->fast_mem = fast_mem;
+    h->stream = stream ? static_cast<cudaStream_t>(stream) : peer->stream;
+    h->procs = peer->procs;
+    h->transport = peer->transport;  // same ranks, same NCCL communicator (and split cache)
+    Pipeline pipe = make_pipeline(make_spec(einsum, dims), h->procs, fast_mem);
     h->exec = std::make_unique<gpu::ScheduleExecutor>(std::move(pipe), h->transport.get(),
                                                       h->stream);
     *out = h.release();

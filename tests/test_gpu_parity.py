@@ -307,9 +307,30 @@ def test_share_input_across_modes(eb):
                     ex0 = ex
             else:
                 if P == 4:
+                    ex = eb.Executor(e, ext, like=ex0)  # same ranks / transport as mode 0
                     ex.share_input(0, ex0, 0)
                     ex.stage([None] + ops[1:])
                 else:
                     ex.stage(ops)
             ex.run()
             check(ex.gather(), oracle.naive_evaluate(e, ext, ops))
+
+
+def test_nccl_transport_single_rank(eb):
+    """The one-process-per-GPU transport (NCCL communicator from a unique id,
+    rank 0 of 1) runs the schedule and gathers on rank 0.  Multi-rank NCCL
+    needs several GPUs; the exchange logic is covered by the gloo tests."""
+    ext = dict(i=32, j=24, k=20, a=8)
+    e = "ijk,ja,ka->ia"
+    ops = oracle.seeded_inputs(e, ext, 4)
+    nid = eb.Executor.nccl_unique_id()
+    assert len(nid) == 128
+    ex = eb.Executor(e, ext, 1, 1024.0, rank=0, nccl_id=nid)
+    ex2 = eb.Executor("ijk,ia,ka->ja", ext, like=ex)
+    ex.stage(ops)
+    ex.run()
+    check(ex.gather(), oracle.naive_evaluate(e, ext, ops))
+    ops2 = oracle.seeded_inputs("ijk,ia,ka->ja", ext, 4)
+    ex2.stage(ops2)
+    ex2.run()
+    check(ex2.gather(), oracle.naive_evaluate("ijk,ia,ka->ja", ext, ops2))
