@@ -477,51 +477,61 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   }
 }
 
-// Deterministic split-K finish: out[m][col0+n] = sum over CTAs (ascending),
-// then over the CTA's k-split groups, of their partial slot for tile m / MT.
-__global__ void reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out,
-                                       int64_t M, int R, int col0, int64_t ldo, int NP, int MT,
-                                       int KS, int64_t per_tile, int64_t items, int G,
-                                       int segmax) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= M * NP) return;
-  const int64_t m = idx / NP;
-  const int n = (int)(idx % NP);
-  if (col0 + n >= R) return;
+// Deterministic split-K finish: out[m][col0+n] = sum over the CTAs whose item
+// range touches row tile m / MT (ascending), and over their SPL partial slots
+// (k-split x outer-index groups).  One block per output row: thread (g, n)
+// sums every kGroups-th contribution of column n with batched independent
+// loads, then the kGroups partial sums are added in fixed order — the result
+// is bitwise reproducible and no FP64 atomics are used.
+constexpr int kReduceGroups = 8;
+
+__global__ void __launch_bounds__(kReduceGroups * 64)
+    reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out, int64_t M,
+                           int R, int col0, int64_t ldo, int NP, int MT, int SPL,
+                           int64_t per_tile, int64_t items, int G, int segmax) {
+  __shared__ double part[kReduceGroups][64];
+  const int64_t m = blockIdx.x;
+  const int n = threadIdx.x % 64, grp = threadIdx.x / 64;
   const int64_t t = m / MT;
   const int64_t lo = t * per_tile, hi = lo + per_tile;
   // CTAs c with [c*items/G, (c+1)*items/G) overlapping [lo, hi):
   //   c >= ceil((lo+1)*G/items) - 1  and  c <= ceil(hi*G/items) - 1.
   const int64_t cmin = ((lo + 1) * G + items - 1) / items - 1;
   const int64_t cmax = (hi * G + items - 1) / items - 1;
-  // Gather the contributions in batches of independent loads (the partial
-  // slots are read once; a serial load->add chain would be latency-bound),
-  // then add them in ascending (CTA, k-split) order.
-  constexpr int kBatch = 16;
-  double acc = 0.0;
   const int64_t cbeg = cmin < 0 ? 0 : cmin;
   const int64_t cend = (cmax < G - 1 ? cmax : G - 1) + 1;
-  const int64_t total = (cend - cbeg) * KS;
-  for (int64_t b = 0; b < total; b += kBatch) {
-    double v[kBatch];
+  const int64_t total = (cend - cbeg) * SPL;
+  double acc = 0.0;
+  if (n < NP) {
+    constexpr int kBatch = 8;
+    for (int64_t b = grp; b < total; b += kReduceGroups * kBatch) {
+      double v[kBatch];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      v[u] = 0.0;
-      const int64_t e = b + u;
-      if (e < total) {
-        const int64_t c = cbeg + e / KS;
-        const int k = (int)(e % KS);
-        const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
-        if (!(c1 <= lo || c0 >= hi || c1 <= c0)) {
-          const int64_t sg = t - c0 / per_tile;
-          v[u] = ws[(((c * segmax + sg) * KS + k) * MT + (m % MT)) * NP + n];
+      for (int u = 0; u < kBatch; ++u) {
+        v[u] = 0.0;
+        const int64_t e = b + (int64_t)u * kReduceGroups;
+        if (e < total) {
+          const int64_t c = cbeg + e / SPL;
+          const int k = (int)(e % SPL);
+          const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
+          if (!(c1 <= lo || c0 >= hi || c1 <= c0)) {
+            const int64_t sg = t - c0 / per_tile;
+            v[u] = ws[(((c * segmax + sg) * SPL + k) * MT + (m % MT)) * NP + n];
+          }
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) acc += v[u];
+      for (int u = 0; u < kBatch; ++u) acc += v[u];
+    }
   }
-  out[m * ldo + col0 + n] = acc;
+  part[grp][n] = acc;
+  __syncthreads();
+  if (grp == 0 && n < NP && col0 + n < R) {
+    double s = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < kReduceGroups; ++g2) s += part[g2][n];
+    out[m * ldo + col0 + n] = s;
+  }
 }
 
 // Uᵀ staging for the ROW variant (TMA needs k innermost): ut[n][l] = u[l][col0+n].
@@ -829,8 +839,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     launch_variant(p, nt, xmap, umap, q, st);
     if (!p.batched) {
       const int np = nt * 8;
-      const int64_t n = d->M * np;
-      reduce_partials_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(
+      reduce_partials_kernel<<<(unsigned)d->M, kReduceGroups * 64, 0, st>>>(
           part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks * p.os, p.O * p.KC, p.items, p.G,
           p.segmax);
       EB_CUDA(cudaGetLastError());
