@@ -327,6 +327,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "virtual", "nccl"],
+                    help="auto: NCCL (one process per GPU) when WORLD_SIZE > 1, else the "
+                         "in-device virtual-rank transport; nccl forces the NCCL path")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -347,18 +350,21 @@ def main():
     L = _capi.lib()
 
     label, modes, scaling = workload(args.config, P)
+    use_nccl = world > 1 or args.transport == "nccl"
     nccl_id = None
     if world > 1:
         obj = [eb.Executor.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif use_nccl:
+        nccl_id = eb.Executor.nccl_unique_id()
     stream = torch.cuda.Stream()
     execs, inputs, grids, flops_tree = [], [], [], 0
     x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
     for mi, (e, ext, build) in enumerate(modes):
         ins = build(pinned=(world == 1)) if mi == 0 else None
         if mi == 0:
-            ex = eb.Executor(e, ext, P, 1024.0, rank if world > 1 else -1, nccl_id,
+            ex = eb.Executor(e, ext, P, 1024.0, rank if use_nccl else -1, nccl_id,
                              stream=stream.cuda_stream)
         else:  # same ranks / same NCCL communicator as mode 0
             ex = eb.Executor(e, ext, stream=stream.cuda_stream, like=execs[0])
@@ -429,7 +435,7 @@ def main():
         h2d = 0
         for ins, ex_, sh in zip(inputs, execs, x_shared):
             # bytes this rank copies: its blocks of every operand it stages
-            h2d += _staged_bytes(ex_, ins, P, rank if world > 1 else -1, eb, skip0=sh)
+            h2d += _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh)
         d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
         reps = max(1, min(args.steps, 3))
         if world > 1:
@@ -486,6 +492,7 @@ def main():
         "data": "synthetic: reference random_tensor streams (mt19937_64, seed 0 for X, "
                 "factor seeds 1/2/3), generated on the host",
         "config": {"workload": label, "procs": P, "fast_mem": 1024, "grids": grids,
+                   "transport": "nccl" if use_nccl else "virtual",
                    "tree_flops_per_step": flops_tree,
                    "l2": "inputs larger than L2 (X is 8.6 GB vs 126 MB L2), no flush needed"},
         "roofline": roof,
