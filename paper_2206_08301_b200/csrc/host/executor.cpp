@@ -646,14 +646,40 @@ void ScheduleExecutor::execute() {
         const auto& src = store_.at({rec->from_term, a.tensor});
         std::vector<DevBlock> dst(static_cast<std::size_t>(procs));
         const TensorPlacement& dp = rec->plan.destination;
+        // A rank whose only incoming message is a self message covering its
+        // whole (identically shaped) block keeps the producer's buffer: the
+        // reference copies it (apply_plan), the result is the same block.
+        std::vector<int> incoming(static_cast<std::size_t>(procs), 0);
+        std::vector<const Message*> only(static_cast<std::size_t>(procs), nullptr);
+        for (const Message& m : rec->plan.messages) {
+          ++incoming[static_cast<std::size_t>(m.dst_rank)];
+          only[static_cast<std::size_t>(m.dst_rank)] = &m;
+        }
+        std::vector<char> alias(static_cast<std::size_t>(procs), 0);
         for (std::int64_t r : owned_) {
           DevBlock& b = dst[static_cast<std::size_t>(r)];
           const auto bc = dp.block_coords_of(r);
           b.shape = dp.dist.shape_of(bc);
           b.base = dp.dist.base_of(bc);
-          b.ptr = run_arena_.alloc(prod(b.shape), stream_, true);
+          const Message* m = only[static_cast<std::size_t>(r)];
+          const DevBlock& sb = src[static_cast<std::size_t>(r)];
+          bool whole = incoming[static_cast<std::size_t>(r)] == 1 && m->self &&
+                       m->src_rank == r && sb.ptr && sb.shape == b.shape;
+          for (std::size_t d = 0; whole && d < b.shape.size(); ++d)
+            whole = m->oy_lo[d] == 0 && m->ox_lo[d] == 0 && m->oy_hi[d] == b.shape[d] &&
+                    m->ox_hi[d] == b.shape[d];
+          if (whole) {
+            alias[static_cast<std::size_t>(r)] = 1;
+            b.ptr = sb.ptr;
+          } else {
+            b.ptr = run_arena_.alloc(prod(b.shape), stream_, true);
+          }
         }
-        transport_->redistribute(rec->plan, src, dst, stream_);
+        RedistributionPlan todo = rec->plan;
+        todo.messages.clear();
+        for (const Message& m : rec->plan.messages)
+          if (!(m.self && alias[static_cast<std::size_t>(m.dst_rank)])) todo.messages.push_back(m);
+        if (!todo.messages.empty()) transport_->redistribute(todo, src, dst, stream_);
         comm_.events.push_back(
             {"redistribute", term.index, a.tensor, rec->plan.transmitted_volume});
         comm_.redistribute_volume += rec->plan.transmitted_volume;

@@ -98,17 +98,26 @@ struct BoxParams {
   double* dst;
 };
 
+// threadIdx.x / blockIdx.x walk the innermost (contiguous) run of the box,
+// blockIdx.y (grid-stride) the outer rows: one row decomposition per block
+// row instead of per element.
 __global__ void copy_box_kernel(const BoxParams b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b.total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i, so = b.soff, dof = b.doff;
-    for (int d = b.nd - 1; d >= 0; --d) {
+  const int nd = b.nd;
+  const int64_t run = nd > 0 ? b.len[nd - 1] : 1;
+  const int64_t rows = b.total / (run > 0 ? run : 1);
+  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+    int64_t r = row, so = b.soff, dof = b.doff;
+    for (int d = nd - 2; d >= 0; --d) {
       const int64_t c = r % b.len[d];
       r /= b.len[d];
       so += c * b.sstride[d];
       dof += c * b.dstride[d];
     }
-    b.dst[dof] = b.src[so];
+    const double* src = b.src + so;
+    double* dst = b.dst + dof;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < run;
+         i += (int64_t)gridDim.x * blockDim.x)
+      dst[i] = src[i];
   }
 }
 
@@ -241,7 +250,11 @@ extern "C" int eb_copy_box(int nd, const double* src, const int64_t* src_shape, 
       ds *= dst_shape[d];
       b.total *= b.len[d];
     }
-    eb::copy_box_kernel<<<eb::grid_for(b.total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    const int64_t run = nd > 0 ? b.len[nd - 1] : 1;
+    const int64_t rows = b.total / run;
+    dim3 grid((unsigned)std::min<int64_t>((run + 255) / 256, 64),
+              (unsigned)std::min<int64_t>(rows, 65535));
+    eb::copy_box_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
     EB_CUDA(cudaGetLastError());
     eb::count_launch();
   });
