@@ -210,3 +210,30 @@ def ref_run(einsum: str, extents: dict, procs: int, operands, fast_mem: float = 
                  _ptr(res), ctypes.byref(secs), comm):
         raise RuntimeError(R.ref_last_error().decode())
     return res, secs.value, (comm[0], comm[1], comm[2])
+
+
+def ref_run_json(einsum: str, extents: dict, procs: int, fast_mem: float = 1024.0,
+                 seed: int = 0, verify: bool = True):
+    """The reference's own C ABI einplan_run_json (capi.cpp:169-226)."""
+    R = ref()
+    R.einplan_session_create.argtypes = [ctypes.c_char_p, ctypes.c_char_p,
+                                         ctypes.POINTER(ctypes.c_void_p)]
+    R.einplan_run_json.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                   ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p,
+                                   ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    R.einplan_free.argtypes = [ctypes.c_void_p]
+    R.einplan_session_destroy.argtypes = [ctypes.c_void_p]
+    R.einplan_last_error.restype = ctypes.c_char_p
+    s = ctypes.c_void_p()
+    if R.einplan_session_create(einsum.encode(), dims_string(extents).encode(), ctypes.byref(s)):
+        raise RuntimeError(R.einplan_last_error().decode())
+    p = ctypes.c_void_p()
+    st = R.einplan_run_json(s, procs, fast_mem, seed, int(verify), None, None, ctypes.byref(p))
+    try:
+        if not p:
+            raise RuntimeError(R.einplan_last_error().decode())
+        return st, ctypes.string_at(p).decode()
+    finally:
+        if p:
+            R.einplan_free(p)
+        R.einplan_session_destroy(s)

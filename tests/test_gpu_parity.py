@@ -334,3 +334,24 @@ def test_nccl_transport_single_rank(eb):
     ex2.stage(ops2)
     ex2.run()
     check(ex2.gather(), oracle.naive_evaluate("ijk,ia,ka->ja", ext, ops2))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("name,einsum,ext", DESK, ids=[d[0] for d in DESK])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_run_report_matches_reference_report(eb, name, einsum, ext, P):
+    """our einplan_run_json report (GPU execution) against the
+    reference's own einplan_run_json on the same session: every field is
+    identical (tree, partition, schedule, comm volumes, verification verdict,
+    output shape) except the floating-point ones, which agree to tolerance."""
+    st, mine = eb.Session(einsum, ext).run_json(P, 1024.0, seed=7, verify=True)
+    rst, theirs = oracle.ref_run_json(einsum, ext, P, 1024.0, seed=7, verify=True)
+    assert st == rst == 0
+    a, b = json.loads(mine), json.loads(theirs)
+    sa, sb = a["output"].pop("sum"), b["output"].pop("sum")
+    assert abs(sa - sb) <= 1e-11 * max(1.0, abs(sb))
+    ea = a["verification"].pop("max_rel_error")
+    eb_ = b["verification"].pop("max_rel_error")
+    assert ea <= 1e-10 and eb_ <= 1e-10
+    assert list(a.keys()) == list(b.keys())
+    assert a == b
