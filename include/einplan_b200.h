@@ -78,6 +78,25 @@ size_t eb_contract_workspace(const eb_contract_desc* d);
 int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* Fused TTM pair: the two TTM steps of one fused term with the intermediate
+ * kept on chip (TTMc-O5 terms [t0,t1] and [t2,out]; replaces two
+ * local_contract calls, proj/src/executor.cpp:220-235):
+ *   out[p][m][b][c] = sum_{j,k} X[p][j][k][m] * U1[j][b] * U2[k][c]
+ * i.e. t0[p][k][m][b] = sum_j X U1 followed by out = sum_k t0 U2.
+ * X row-major [P][Q1][Q2][M], U1 [Q1][ldu1], U2 [Q2][ldu2], out
+ * [P][M][N1][N2].  Needs Q1 <= 64, N1 <= 16, N2 <= 16, M even; no workspace. */
+typedef struct eb_ttm2_desc {
+  int64_t P, Q1, Q2, M, N1, N2;
+  const double* X;
+  const double* U1;
+  int64_t ldu1;
+  const double* U2;
+  int64_t ldu2;
+  double* out;
+} eb_ttm2_desc;
+
+int eb_ttm2(const eb_ttm2_desc* d, void* stream);
+
 /* Generic binary (or unary) einsum step on dense row-major device blocks:
  * out[...] = sum over contracted symbols of lhs[...] * rhs[...] — the GPU
  * replacement of naive_evaluate for step shapes the fused kernels do not

@@ -33,6 +33,15 @@ class ContractDesc(ctypes.Structure):
     ]
 
 
+class Ttm2Desc(ctypes.Structure):
+    _fields_ = [
+        ("P", ctypes.c_int64), ("Q1", ctypes.c_int64), ("Q2", ctypes.c_int64),
+        ("M", ctypes.c_int64), ("N1", ctypes.c_int64), ("N2", ctypes.c_int64),
+        ("X", ctypes.c_void_p), ("U1", ctypes.c_void_p), ("ldu1", ctypes.c_int64),
+        ("U2", ctypes.c_void_p), ("ldu2", ctypes.c_int64), ("out", ctypes.c_void_p),
+    ]
+
+
 EB_ROW, EB_COL = 0, 1
 EB_REDUCE, EB_BATCHED = 0, 1
 
@@ -45,7 +54,8 @@ EXPORTS = [
     "einplan_version", "einplan_status_name", "einplan_last_error", "einplan_free",
     "einplan_session_create", "einplan_session_destroy", "einplan_bound_json",
     "einplan_plan_json", "einplan_run_json", "einplan_bench_json",
-    "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_step_generic",
+    "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_ttm2",
+    "eb_step_generic",
     "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
@@ -95,6 +105,7 @@ def lib():
         _sig(L, "eb_contract_workspace", ctypes.c_size_t, [ctypes.POINTER(ContractDesc)])
         _sig(L, "eb_contract", ctypes.c_int,
              [ctypes.POINTER(ContractDesc), _vp, ctypes.c_size_t, _vp])
+        _sig(L, "eb_ttm2", ctypes.c_int, [ctypes.POINTER(Ttm2Desc), _vp])
         _sig(L, "eb_random_fill_host", None, [_dp, _i64, ctypes.c_uint64, _i64])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,

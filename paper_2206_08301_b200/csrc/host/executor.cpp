@@ -54,6 +54,57 @@ std::int64_t prod(const std::vector<std::int64_t>& v) {
   return n;
 }
 
+// Copy the dense device block (shape, base) to / from its box inside the
+// row-major host tensor of shape gshape (scatter / gather, executor.cpp:48-78).
+// Trailing dims the block spans completely collapse into one contiguous run;
+// the next dim becomes the height of a pitched 2D copy; only the dims above
+// it are looped over on the host.
+void copy_box_host(bool h2d, double* host, const std::vector<std::int64_t>& gshape,
+                   const std::vector<std::int64_t>& shape, const std::vector<std::int64_t>& base,
+                   double* dev, cudaStream_t st) {
+  const std::size_t nd = gshape.size();
+  const cudaMemcpyKind kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  if (nd == 0 || prod(shape) == 0) {
+    if (nd == 0)
+      cuda_ok(h2d ? cudaMemcpyAsync(dev, host, 8, kind, st) : cudaMemcpyAsync(host, dev, 8, kind, st),
+              "box copy");
+    return;
+  }
+  std::vector<std::int64_t> gstr(nd, 1);
+  for (std::size_t d = nd; d-- > 1;) gstr[d - 1] = gstr[d] * gshape[d];
+  std::size_t d0 = nd - 1;  // every dim after d0 is spanned completely
+  while (d0 > 0 && shape[d0] == gshape[d0]) --d0;
+  const std::int64_t run = shape[d0] * gstr[d0];
+  const std::size_t run_b = static_cast<std::size_t>(run) * 8;
+  if (d0 == 0) {
+    double* h = host + base[0] * gstr[0];
+    cuda_ok(h2d ? cudaMemcpyAsync(dev, h, run_b, kind, st) : cudaMemcpyAsync(h, dev, run_b, kind, st),
+            "box copy");
+    return;
+  }
+  const std::size_t dh = d0 - 1;  // pitched-copy dim
+  const std::int64_t height = shape[dh];
+  const std::size_t hpitch = static_cast<std::size_t>(gstr[dh]) * 8;
+  std::int64_t groups = 1;
+  for (std::size_t d = 0; d < dh; ++d) groups *= shape[d];
+  std::vector<std::int64_t> idx(dh, 0);
+  for (std::int64_t gi = 0; gi < groups; ++gi) {
+    std::int64_t off = base[dh] * gstr[dh] + base[d0] * gstr[d0];
+    for (std::size_t d = 0; d < dh; ++d) off += (base[d] + idx[d]) * gstr[d];
+    double* dv = dev + gi * height * run;
+    double* h = host + off;
+    cuda_ok(h2d ? cudaMemcpy2DAsync(dv, run_b, h, hpitch, run_b, static_cast<std::size_t>(height),
+                                    kind, st)
+                : cudaMemcpy2DAsync(h, hpitch, dv, run_b, run_b, static_cast<std::size_t>(height),
+                                    kind, st),
+            "box copy 2D");
+    for (std::size_t d = dh; d-- > 0;) {
+      if (++idx[d] < shape[d]) break;
+      idx[d] = 0;
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- buffers --
@@ -368,48 +419,7 @@ void ScheduleExecutor::share_input(int k, const ScheduleExecutor& src, int k_src
 
 void ScheduleExecutor::copy_block_h2d(const double* global, const std::vector<std::int64_t>& gshape,
                                       const DevBlock& b) {
-  const std::int64_t n = prod(b.shape);
-  if (n == prod(gshape)) {  // the whole tensor: one copy straight from the caller
-    cuda_ok(cudaMemcpyAsync(b.ptr, global, static_cast<std::size_t>(n) * 8,
-                            cudaMemcpyHostToDevice, stream_),
-            "H2D");
-    return;
-  }
-  // Strided block: copy contiguous innermost runs with a 2D memcpy per
-  // leading index (cudaMemcpy2DAsync handles the row pitch).
-  const std::size_t nd = gshape.size();
-  std::vector<std::int64_t> gstr(nd, 1);
-  for (std::size_t d = nd; d-- > 1;) gstr[d - 1] = gstr[d] * gshape[d];
-  const std::int64_t run = b.shape[nd - 1];
-  std::int64_t rows = 1;
-  for (std::size_t d = 0; d + 1 < nd; ++d) rows *= b.shape[d];
-  // Rows of the block enumerate the leading dims row-major; the innermost
-  // run of each row is contiguous in both tensors.
-  if (nd == 1) {
-    cuda_ok(cudaMemcpyAsync(b.ptr, global + b.base[0], static_cast<std::size_t>(run) * 8,
-                            cudaMemcpyHostToDevice, stream_),
-            "H2D");
-    return;
-  }
-  // Group rows by the second-innermost dim: each group is a 2D pitched copy.
-  const std::int64_t inner_rows = b.shape[nd - 2];
-  const std::int64_t groups = rows / inner_rows;
-  std::vector<std::int64_t> idx(nd - 2, 0);
-  for (std::int64_t gidx = 0; gidx < groups; ++gidx) {
-    std::int64_t off = 0;
-    for (std::size_t d = 0; d + 2 < nd; ++d) off += (b.base[d] + idx[d]) * gstr[d];
-    off += b.base[nd - 2] * gstr[nd - 2] + b.base[nd - 1];
-    cuda_ok(cudaMemcpy2DAsync(b.ptr + gidx * inner_rows * run, static_cast<std::size_t>(run) * 8,
-                              global + off, static_cast<std::size_t>(gstr[nd - 2]) * 8,
-                              static_cast<std::size_t>(run) * 8,
-                              static_cast<std::size_t>(inner_rows), cudaMemcpyHostToDevice,
-                              stream_),
-            "H2D 2D");
-    for (std::size_t d = nd - 2; d-- > 0;) {
-      if (++idx[d] < b.shape[d]) break;
-      idx[d] = 0;
-    }
-  }
+  copy_box_host(true, const_cast<double*>(global), gshape, b.shape, b.base, b.ptr, stream_);
 }
 
 const RedistRecord* ScheduleExecutor::find_redist(int to_term, const std::string& t) const {
@@ -548,6 +558,58 @@ bool ScheduleExecutor::try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
   const std::size_t wb = eb_contract_workspace(&d);
   if (wb == 0) return false;
   eb_ok(eb_contract(&d, workspace(wb), wb, stream_), "eb_contract (MTTKRP term)");
+  ++launches_fused_;
+  return true;
+}
+
+// A term of exactly two TTM steps chained through their intermediate,
+//   s0: X[P j k R], U1[j b] -> t0[P k R b]    s1: t0[P k R b], U2[k c] -> out[P R b c]
+// (both TTMc-O5 terms; executor.cpp:220-235 runs them back to back) goes to
+// eb_ttm2 with t0 kept on chip.
+bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
+                                      const std::map<std::string, const DevBlock*>& at_hand,
+                                      DevBlock& out) {
+  if (term.step_ids.size() != 2) return false;
+  const ContractionTree& tree = pipe_.tree;
+  const ContractionStep& s0 = tree.steps[static_cast<std::size_t>(term.step_ids[0])];
+  const ContractionStep& s1 = tree.steps[static_cast<std::size_t>(term.step_ids[1])];
+  if (s0.rhs < 0 || s1.rhs < 0 || s0.rhs_indices.size() != 2 || s1.rhs_indices.size() != 2)
+    return false;
+  if (tree.tensor_name(s1.lhs) != tree.tensor_name(tree.result_id(term.step_ids[0])))
+    return false;
+  if (tree.tensor_name(tree.result_id(term.step_ids[1])) != term.statement.output) return false;
+  const std::string& xi = s0.lhs_indices;
+  const char j = s0.rhs_indices[0], b = s0.rhs_indices[1];
+  const char k = s1.rhs_indices[0], c = s1.rhs_indices[1];
+  const auto pj = xi.find(j);
+  if (pj == std::string::npos || pj + 1 >= xi.size() || xi[pj + 1] != k) return false;
+  if (contains(xi, b) || contains(xi, c) || b == c) return false;
+  const std::string pre = xi.substr(0, pj), rest = xi.substr(pj + 2);
+  if (s0.result_indices != pre + k + rest + b || s1.lhs_indices != s0.result_indices ||
+      s1.result_indices != pre + rest + b + c)
+    return false;
+  eb_ttm2_desc d;
+  std::memset(&d, 0, sizeof(d));
+  d.P = 1;
+  for (char s : pre) d.P *= local_len(term, s, rank);
+  d.M = 1;
+  for (char s : rest) d.M *= local_len(term, s, rank);
+  d.Q1 = local_len(term, j, rank);
+  d.Q2 = local_len(term, k, rank);
+  d.N1 = local_len(term, b, rank);
+  d.N2 = local_len(term, c, rank);
+  if (d.Q1 > 64 || d.N1 > 16 || d.N2 > 16 || d.M % 2 != 0) return false;
+  const DevBlock* x = at_hand.at(tree.tensor_name(s0.lhs));
+  const DevBlock* u1 = at_hand.at(tree.tensor_name(s0.rhs));
+  const DevBlock* u2 = at_hand.at(tree.tensor_name(s1.rhs));
+  d.X = x->ptr;
+  d.U1 = u1->ptr;
+  d.ldu1 = u1->shape[1];
+  d.U2 = u2->ptr;
+  d.ldu2 = u2->shape[1];
+  out = new_block(term, s1.result_indices, rank, false);
+  d.out = out.ptr;
+  eb_ok(eb_ttm2(&d, stream_), "eb_ttm2 (fused TTM pair)");
   ++launches_fused_;
   return true;
 }
@@ -703,7 +765,8 @@ void ScheduleExecutor::execute() {
       std::map<std::string, const DevBlock*> at_hand;
       for (auto& kv : arrays) at_hand[kv.first] = &(*kv.second)[static_cast<std::size_t>(rank)];
       DevBlock result;
-      if (try_fused_mttkrp(term, rank, at_hand, result)) {
+      if (try_fused_mttkrp(term, rank, at_hand, result) ||
+          (fuse_ttm_ && try_fused_ttm2(term, rank, at_hand, result))) {
         out_blocks[static_cast<std::size_t>(rank)] = result;
         continue;
       }
@@ -743,33 +806,13 @@ void ScheduleExecutor::gather(double* host_out) {
     return;  // only rank 0 assembles
   }
   const auto gshape = place.dist.extents;
-  const std::size_t nd = gshape.size();
-  std::vector<std::int64_t> gstr(nd, 1);
-  for (std::size_t d = nd; d-- > 1;) gstr[d - 1] = gstr[d] * gshape[d];
   const std::int64_t procs = place.term_grid.total();
   for (std::int64_t r = 0; r < procs; ++r) {
     if (!place.is_canonical(r)) continue;
     const DevBlock& b = blocks[static_cast<std::size_t>(r)];
     const auto shape = place.dist.shape_of(place.block_coords_of(r));
     const auto base = place.dist.base_of(place.block_coords_of(r));
-    if (nd == 0) {
-      cuda_ok(cudaMemcpyAsync(host_out, b.ptr, 8, cudaMemcpyDeviceToHost, stream_), "D2H");
-      continue;
-    }
-    const std::int64_t run = shape[nd - 1];
-    const std::int64_t rows = prod(shape) / std::max<std::int64_t>(run, 1);
-    std::vector<std::int64_t> idx(nd - 1, 0);
-    for (std::int64_t row = 0; row < rows; ++row) {
-      std::int64_t off = base[nd - 1];
-      for (std::size_t d = 0; d + 1 < nd; ++d) off += (base[d] + idx[d]) * gstr[d];
-      cuda_ok(cudaMemcpyAsync(host_out + off, b.ptr + row * run, static_cast<std::size_t>(run) * 8,
-                              cudaMemcpyDeviceToHost, stream_),
-              "D2H");
-      for (std::size_t d = nd - 1; d-- > 0;) {
-        if (++idx[d] < shape[d]) break;
-        idx[d] = 0;
-      }
-    }
+    copy_box_host(false, host_out, gshape, shape, base, b.ptr, stream_);
   }
   cuda_ok(cudaStreamSynchronize(stream_), "sync");
 }

@@ -1,6 +1,8 @@
 // GPU schedule executor (see executor.cpp).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <map>
@@ -128,6 +130,9 @@ class ScheduleExecutor {
   DevBlock new_block(const TermPlan& term, const std::string& idx, std::int64_t rank, bool zero);
   bool try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
                         const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
+  // Two chained TTM steps of one term on the fused eb_ttm2 kernel.
+  bool try_fused_ttm2(const TermPlan& term, std::int64_t rank,
+                      const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
   DevBlock run_step(const TermPlan& term, int sid, std::int64_t rank,
                     const std::map<std::string, const DevBlock*>& at_hand);
 
@@ -144,6 +149,11 @@ class ScheduleExecutor {
   std::size_t workspace_bytes_ = 0;
   CommStats comm_;
   int launches_fused_ = 0, launches_ttm_ = 0, launches_generic_ = 0;
+  // EB_FUSE_TTM2=0 runs TTM-pair terms as two eb_contract launches (A/B checks)
+  bool fuse_ttm_ = [] {
+    const char* v = std::getenv("EB_FUSE_TTM2");
+    return !(v && v[0] == '0');
+  }();
 };
 
 }  // namespace gpu

@@ -1,0 +1,380 @@
+// Fused TTM pair for B200 (sm_100a): two consecutive TTM steps of one fused
+// term with the intermediate kept on chip.
+//
+// Replaces, for terms whose two steps are
+//   t0[P, k, R, b] = sum_j X[P, j, k, R] U1[j, b]        (TTM, planner.cpp:122-127)
+//   t [P, R, b, c] = sum_k t0[P, k, R, b] U2[k, c]       (TTM on the intermediate)
+// the reference's two naive_evaluate calls per rank (proj/src/evaluate.cpp:7-63
+// via local_contract, proj/src/executor.cpp:126-154, looping over
+// term.step_ids at executor.cpp:220-235).  In the TTMc-O5 schedule both terms
+// have this shape ([t0,t1]: ijklm -> iklmb -> ilmbc, [t2,out]: ilmbc ->
+// imbcd -> ibcde), so t0 (2.1 GB at C5) and t2 never
+// touch HBM: X is read once and only the term's output is written.
+//
+// Data path.  One CTA item = (p, 16-row tile of R).  X streams through a
+// 6-deep TMA ring; one stage is the box X[p, 0:64, k:k+4, r:r+16] (32 KB,
+// SWIZZLE_128B, j fastest among the 128-B rows).  8 consumer warps:
+//   step 0  warp (kk, jh) contracts j in [32jh, 32jh+32) for k = 4*kc + kk and
+//           all 16 rows on DMMA (mma.sync.m8n8k4.f64; 2 row x 2 column tiles =
+//           four independent accumulator chains; U1 held in registers),
+//           releases the stage and writes its partial t0 to a double-buffered
+//           smem tile [jh][kk][r][b];
+//   step 1  after one named barrier, warp w accumulates rows 2w, 2w+1 of the
+//           output tile: out[r][b][c] += sum_{k in stage} t0[k][r][b] U2[k][c]
+//           (a second DMMA whose A operand is the sum of the two j halves).
+// Per stage: 256 + 64 DMMA.8x8x4 for 32 KB of X — at the FP64/HBM ridge, so
+// both pipes must run near peak together.
+//
+// Bank conflicts.  Step-0 A fragments: lane (g, l) reads X[j = perm(s, l)][r = g]
+// with perm(s, l) = 2l + (s&1) + 8(s>>1) (shared with the U1 fragment, so the
+// contraction is unchanged); rows j of a half-warp differ by {0,2,4,6} in their
+// swizzle phase, which spreads the 2 chunks x 4 rows over 8 distinct 16-B bank
+// groups.  The t0 tile [kk][r][b] (128-B rows) is stored with chunk
+// c ^ 4(r&1) ^ 2kk: conflict-free for the double2 writes (two rows per
+// quarter-warp) and for the step-1 reads (four kk planes per half-warp).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "../host/status.hpp"
+#include "device_common.cuh"
+#include "einplan_b200.h"
+#include "tma_host.hpp"
+
+namespace eb {
+
+namespace {
+
+constexpr int kRows = 16;                          // R rows per item
+constexpr int kJ = 64;                             // whole j range per stage (Q1 <= 64)
+constexpr int kK = 4;                              // k values per stage
+constexpr int kNB = 16;                            // max N1 / N2
+constexpr int kXBytes = kRows * kJ * kK * 8;       // 32 KB
+constexpr int kPlane = kRows * kNB * 8;            // one (j part, k) t0 plane: 2 KB
+
+// NW consumer warps: step 0 splits j into JP = NW/4 parts (warp = (k, j part),
+// 16 rows x 16 columns = four DMMA chains); step 1 gives each warp RW = 16/NW
+// output rows.  More warps = more independent chains per SM sub-partition.
+template <int NW>
+struct Cfg {
+  static constexpr int JP = NW / 4;
+  static constexpr int JW = kJ / JP;   // j per warp
+  static constexpr int B16 = JW / 16;  // 16-deep j groups per warp
+  static constexpr int RW = kRows / NW;
+  static constexpr int T0Bytes = JP * kK * kPlane;
+  static constexpr int Stages = NW == 8 ? 6 : 5;
+  static constexpr int Smem = Stages * kXBytes + 2 * T0Bytes + 1024;
+  static_assert(NW == 8 || NW == 16, "8 or 16 consumer warps");
+};
+
+struct Ttm2Params {
+  int64_t P, Q1, Q2, M, N1, N2;
+  int64_t mtiles, items, KC;
+  int G;
+  const double* U1;
+  int64_t ldu1;
+  const double* U2;
+  int64_t ldu2;
+  double* out;
+};
+
+template <int NW>
+__device__ __forceinline__ void consumer_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
+
+template <int NW, bool PIPE>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    ttm2_kernel(const __grid_constant__ CUtensorMap xmap, const Ttm2Params prm) {
+  using C = Cfg<NW>;
+  constexpr int S = C::Stages;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[S];
+  __shared__ __align__(8) uint64_t empty_bar[S];
+
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+  uint8_t* const t0s = sbase + S * kXBytes;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_addr(&full_bar[s]), 1);
+      mbar_init(smem_addr(&empty_bar[s]), NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch_desc(&xmap);
+      uint32_t it = 0;
+      for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+        const int p = (int)(item / prm.mtiles);
+        const int r0 = (int)(item % prm.mtiles) * kRows;
+        for (int64_t kc = 0; kc < prm.KC; ++kc, ++it) {
+          const int st = it % S;
+          if (it >= (uint32_t)S) mbar_wait(smem_addr(&empty_bar[st]), ((it / S) - 1) & 1);
+          const uint32_t fb = smem_addr(&full_bar[st]);
+          mbar_expect_tx(fb, kXBytes);
+          // map dims {M, Q1, Q2, P}: box {16, 64, 4, 1} -> smem [kk][j][16 r]
+          tma_load_4d(base + st * kXBytes, &xmap, fb, r0, 0, (int)(kc * kK), p);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int g = lane >> 2, l = lane & 3;
+  const int kk = warp / C::JP, jp = warp % C::JP;  // step 0: k = 4kc + kk, j in part jp
+
+  // U1 B fragments of this warp's j part: [16-group][k4 step][n8 tile].
+  double u1[C::B16][4][2];
+#pragma unroll
+  for (int b16 = 0; b16 < C::B16; ++b16)
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int64_t j = C::JW * jp + 16 * b16 + 2 * l + (s & 1) + 8 * (s >> 1);
+        const int64_t n = 8 * nj + g;
+        u1[b16][s][nj] = (j < prm.Q1 && n < prm.N1) ? __ldg(prm.U1 + j * prm.ldu1 + n) : 0.0;
+      }
+
+  // step-0 A offsets inside a stage for rows 8mi + g (b16 = 0; +b16 * 16 rows of 128 B)
+  uint32_t offa[4][2];
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int j = C::JW * jp + 2 * l + (s & 1) + 8 * (s >> 1);
+      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (j & 7));
+      offa[s][mi] = (uint32_t)(kk * kJ + j) * 128u + chunk * 16u + (g & 1) * 8u;
+    }
+  // partial-t0 writes: plane (jp, kk), row r = 8mi + g, columns 8nj + 2l, +1
+  uint32_t offw[2][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      const int r = 8 * mi + g;
+      const uint32_t chunk = (uint32_t)((4 * nj + l) ^ (4 * (r & 1)) ^ (2 * kk));
+      offw[mi][nj] = (uint32_t)(jp * kK + kk) * kPlane + (uint32_t)r * 128u + chunk * 16u;
+    }
+  // step-1 A reads: planes (jp', kk' = l) for every j part, row r = RW*w + ri, column b = 8mi + g
+  uint32_t offr[C::RW][2];
+#pragma unroll
+  for (int ri = 0; ri < C::RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = C::RW * warp + ri;
+      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (4 * (r & 1)) ^ (2 * l));
+      offr[ri][mi] = (uint32_t)l * kPlane + (uint32_t)r * 128u + chunk * 16u + (g & 1) * 8u;
+    }
+
+  double acc[C::RW][2][2][2];  // output tile rows RW*w+ri: [ri][mi (b)][nj (c)][2]
+#pragma unroll
+  for (int ri = 0; ri < C::RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+
+  // U2 B fragments of stage kc (k = 4kc + l, c = 8nj + g)
+  auto load_u2 = [&](int64_t kc, double (&ub)[2]) {
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      const int64_t k = kc * kK + l, c = 8 * nj + g;
+      ub[nj] = (k < prm.Q2 && c < prm.N2) ? __ldg(prm.U2 + k * prm.ldu2 + c) : 0.0;
+    }
+  };
+  double ub[2] = {0.0, 0.0};  // fragments of the stage whose step 1 is pending
+
+  // Step 1 of stage s runs one stage late, after step 0 of stage s + 1: its
+  // t0 operands are loaded before that step 0 (latency hidden under its
+  // DMMAs) and one named barrier per stage (after the t0 write) orders the
+  // double-buffered t0 tile.
+  double t0a[C::RW][2];
+  auto load_t0 = [&](uint32_t stage_it) {
+    const uint8_t* tb = t0s + (stage_it & 1) * C::T0Bytes;
+#pragma unroll
+    for (int ri = 0; ri < C::RW; ++ri)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        double v = *reinterpret_cast<const double*>(tb + offr[ri][mi]);
+#pragma unroll
+        for (int q = 1; q < C::JP; ++q)  // the j-part partials, fixed order
+          v += *reinterpret_cast<const double*>(tb + offr[ri][mi] + q * kK * kPlane);
+        t0a[ri][mi] = v;
+      }
+  };
+  auto step1 = [&](const double (&u)[2]) {
+#pragma unroll
+    for (int ri = 0; ri < C::RW; ++ri)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+          dmma884(acc[ri][mi][nj][0], acc[ri][mi][nj][1], t0a[ri][mi], u[nj]);
+  };
+
+  uint32_t it = 0;
+  for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+    const int64_t p = item / prm.mtiles;
+    const int64_t r0 = (item % prm.mtiles) * kRows;
+    for (int64_t kc = 0; kc < prm.KC; ++kc, ++it) {
+      const int st = it % S;
+      double ub_next[2];
+      load_u2(kc, ub_next);
+      if (PIPE && kc > 0) load_t0(it - 1);
+      mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
+      const uint8_t* xs = sbase + st * kXBytes;
+      double t[2][2][2];  // [mi][nj][2]: four independent DMMA chains
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) t[mi][nj][0] = t[mi][nj][1] = 0.0;
+#pragma unroll
+      for (int b16 = 0; b16 < C::B16; ++b16)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double a[2];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+            a[mi] = *reinterpret_cast<const double*>(xs + offa[s][mi] + b16 * 16 * 128);
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 2; ++nj)
+              dmma884(t[mi][nj][0], t[mi][nj][1], a[mi], u1[b16][s][nj]);
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
+      if (PIPE && kc > 0) step1(ub);  // stage kc - 1
+      ub[0] = ub_next[0];             // now stage kc's fragments
+      ub[1] = ub_next[1];
+
+      uint8_t* tb = t0s + (it & 1) * C::T0Bytes;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+          *reinterpret_cast<double2*>(tb + offw[mi][nj]) = make_double2(t[mi][nj][0], t[mi][nj][1]);
+      consumer_barrier<NW>();
+      if (!PIPE) {
+        load_t0(it);
+        step1(ub);
+      }
+    }
+    if (PIPE) {  // the item's last stage
+      load_t0(it - 1);
+      step1(ub);
+    }
+    // out[p][r][b][c], guarded at ragged rows / N1 / N2
+#pragma unroll
+    for (int ri = 0; ri < C::RW; ++ri) {
+      const int64_t r = r0 + C::RW * warp + ri;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int64_t b = 8 * mi + g;
+        if (r < prm.M && b < prm.N1) {
+          double* dst = prm.out + ((p * prm.M + r) * prm.N1 + b) * prm.N2;
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) {
+            const int64_t c = 8 * nj + 2 * l;
+            if (c + 1 < prm.N2 && (reinterpret_cast<uintptr_t>(dst + c) & 15) == 0) {
+              *reinterpret_cast<double2*>(dst + c) =
+                  make_double2(acc[ri][mi][nj][0], acc[ri][mi][nj][1]);
+            } else {
+              if (c < prm.N2) dst[c] = acc[ri][mi][nj][0];
+              if (c + 1 < prm.N2) dst[c + 1] = acc[ri][mi][nj][1];
+            }
+          }
+        }
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+      }
+    }
+  }
+}
+
+void validate(const eb_ttm2_desc* d) {
+  if (!d) throw InvalidError("eb_ttm2: null descriptor");
+  if (d->P < 1 || d->Q1 < 1 || d->Q2 < 1 || d->M < 1 || d->N1 < 1 || d->N2 < 1)
+    throw InvalidError("eb_ttm2: extents must be positive");
+  if (d->Q1 > kJ || d->N1 > kNB || d->N2 > kNB)
+    throw InvalidError("eb_ttm2: needs Q1 <= 64, N1 <= 16, N2 <= 16");
+  if (d->M % 2 != 0) throw InvalidError("eb_ttm2: innermost X extent must be even (TMA 16-B pitch)");
+  if (!d->X || !d->U1 || !d->U2 || !d->out) throw InvalidError("eb_ttm2: null tensor");
+  if (d->ldu1 < d->N1 || d->ldu2 < d->N2) throw InvalidError("eb_ttm2: bad factor leading dims");
+}
+
+template <int NW, bool PIPE>
+void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    EB_CUDA(cudaFuncSetAttribute(ttm2_kernel<NW, PIPE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NW>::Smem));
+    attr = true;
+  }
+  main_kernel_begin(st);
+  ttm2_kernel<NW, PIPE><<<prm.G, (NW + 1) * 32, Cfg<NW>::Smem, st>>>(xmap, prm);
+  EB_CUDA(cudaGetLastError());
+  main_kernel_end(st);
+  count_launch();
+}
+
+void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
+  validate(d);
+  check_device();
+  Ttm2Params prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.P = d->P;
+  prm.Q1 = d->Q1;
+  prm.Q2 = d->Q2;
+  prm.M = d->M;
+  prm.N1 = d->N1;
+  prm.N2 = d->N2;
+  prm.mtiles = (d->M + kRows - 1) / kRows;
+  prm.items = d->P * prm.mtiles;
+  prm.KC = (d->Q2 + kK - 1) / kK;
+  prm.G = (int)std::min<int64_t>(prm.items, (int64_t)sm_count());
+  prm.U1 = d->U1;
+  prm.ldu1 = d->ldu1;
+  prm.U2 = d->U2;
+  prm.ldu2 = d->ldu2;
+  prm.out = d->out;
+  // X dims {M, Q1, Q2, P} (j before k so the 128-B box rows run over j)
+  const uint64_t dims[4] = {(uint64_t)d->M, (uint64_t)d->Q1, (uint64_t)d->Q2, (uint64_t)d->P};
+  const uint64_t str[3] = {(uint64_t)(d->Q2 * d->M) * 8, (uint64_t)d->M * 8,
+                           (uint64_t)(d->Q1 * d->Q2 * d->M) * 8};
+  const uint32_t box[4] = {16, (uint32_t)kJ, (uint32_t)kK, 1};
+  const CUtensorMap xmap = make_map(d->X, 4, dims, str, box);
+  // tuning knobs (A/B measurements): consumer warps 8 / 16, step-1 pipelining
+  const char* v = std::getenv("EB_TTM2_WARPS");
+  const char* pp = std::getenv("EB_TTM2_PIPE");
+  // (measured, C5 terms at 1965 MHz: 8 warps unpipelined 1.56 ms, pipelined
+  // 1.60, 16 warps 1.73 / 2.19 — tools/ttm2_bench.py)
+  const bool pipe = pp && pp[0] == '1';
+  if (v && std::atoi(v) == 16)
+    pipe ? launch<16, true>(xmap, prm, st) : launch<16, false>(xmap, prm, st);
+  else
+    pipe ? launch<8, true>(xmap, prm, st) : launch<8, false>(xmap, prm, st);
+}
+
+}  // namespace
+
+}  // namespace eb
+
+extern "C" int eb_ttm2(const eb_ttm2_desc* d, void* stream) {
+  return eb::guard([&] { eb::run_ttm2(d, static_cast<cudaStream_t>(stream)); });
+}

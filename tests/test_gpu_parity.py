@@ -104,6 +104,76 @@ def test_contract_ttm(eb, I, J, K, B):
     check(got, want)
 
 
+TTM2_SHAPES = [(2, 64, 64, 64, 16, 16), (3, 40, 7, 50, 16, 16), (1, 64, 9, 18, 5, 11),
+               (4, 3, 130, 2, 16, 1), (2, 33, 64, 34, 8, 16), (1, 1, 1, 2, 1, 1),
+               (5, 64, 4, 16, 16, 16)]
+
+
+@pytest.mark.parametrize("P,Q1,Q2,M,N1,N2", TTM2_SHAPES)
+def test_ttm2_pair(eb, P, Q1, Q2, M, N1, N2):
+    """eb_ttm2 = the two chained TTM steps pjkm,jb->pkmb ; pkmb,kc->pmbc of one
+    term (TTMc-O5), ragged in every extent, against the oracle's n-ary loop."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    e = "pjkm,jb,kc->pmbc"
+    ext = dict(p=P, j=Q1, k=Q2, m=M, b=N1, c=N2)
+    ops = oracle.seeded_inputs(e, ext, 23)
+    want = oracle.naive_evaluate(e, ext, ops)
+    X, U1, U2 = [torch.from_numpy(o).cuda() for o in ops]
+    out = torch.full(want.shape, float("nan"), dtype=torch.float64, device="cuda")
+    d = C.Ttm2Desc(P, Q1, Q2, M, N1, N2, X.data_ptr(), U1.data_ptr(), N1, U2.data_ptr(), N2,
+                   out.data_ptr())
+    C.check(C.lib().eb_ttm2(ctypes.byref(d),
+                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), want)
+
+
+def test_ttm2_rejects_unsupported_shapes(eb):
+    from paper_2206_08301_b200 import _capi as C
+    d = C.Ttm2Desc(1, 65, 4, 16, 16, 16, 8, 8, 16, 8, 16, 8)
+    assert C.lib().eb_ttm2(ctypes.byref(d), None) == 1  # EB_E_INVALID, nothing launched
+    d = C.Ttm2Desc(1, 64, 4, 15, 16, 16, 8, 8, 16, 8, 16, 8)
+    assert C.lib().eb_ttm2(ctypes.byref(d), None) == 1
+
+
+def _ttmc_o5_chain(ext, ops):
+    """The reference tree of TTMc-O5 evaluated step by step with the oracle
+    (ijklm -> iklmb -> ilmbc -> imbcd -> ibcde, Appendix A of SURVEY)."""
+    X, U1, U2, U3, U4 = ops
+    t = oracle.naive_evaluate("ijklm,jb->iklmb", ext, [X, U1])
+    t = oracle.naive_evaluate("iklmb,kc->ilmbc", ext, [t, U2])
+    t = oracle.naive_evaluate("ilmbc,ld->imbcd", ext, [t, U3])
+    return oracle.naive_evaluate("imbcd,me->ibcde", ext, [t, U4])
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_ttmc_o5_fused_terms(eb, P, monkeypatch):
+    """Both TTMc-O5 terms ([t0,t1], [t2,out]: the C5 partition at these
+    extents, with the i2m2 / i2c2 / i2l2m2 / i2b2c2 grids of P=4, 8) run on
+    eb_ttm2 — two fused launches per rank — and match the oracle chain and
+    the unfused two-launch path."""
+    e = "ijklm,jb,kc,ld,me->ibcde"
+    ext = dict(i=16 * P, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12)
+    plan = json.loads(eb.plan_json(e, ext, P))
+    assert [t["output"] for t in plan["schedule"]["terms"]] == ["t1", "out"]
+    ops = oracle.seeded_inputs(e, ext, 5)
+    want = _ttmc_o5_chain(ext, ops)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    ex.run()
+    st = ex.stats()
+    assert st["fused_launches"] == 2 * P and st["ttm_launches"] == 0, st
+    assert st["generic_launches"] == 0, st
+    check(ex.gather(), want)
+    monkeypatch.setenv("EB_FUSE_TTM2", "0")
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    ex.run()
+    assert ex.stats()["ttm_launches"] == 4 * P
+    check(ex.gather(), want)
+
+
 def test_contract_order5_all_krp_rows(eb):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
