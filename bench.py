@@ -327,6 +327,11 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", default="modes", choices=["modes", "dimtree"],
+                    help="C2 only. modes: the reference's three einsums, one schedule each; "
+                         "dimtree: modes 0 and 1 from one pass over X (T = X x_k C folded "
+                         "into both outputs, eb_exec_run_pair), mode 2 as before — 2/3 of "
+                         "the DMMA flops for the same three outputs")
     ap.add_argument("--transport", default="auto", choices=["auto", "virtual", "nccl"],
                     help="auto: NCCL (one process per GPU) when WORLD_SIZE > 1, else the "
                          "in-device virtual-rank transport; nccl forces the NCCL path")
@@ -350,6 +355,12 @@ def main():
     L = _capi.lib()
 
     label, modes, scaling = workload(args.config, P)
+    dimtree = args.sweep == "dimtree"
+    if dimtree and args.config != "C2":
+        raise SystemExit("--sweep dimtree applies to the C2 CP-ALS sweep only")
+    if dimtree:
+        label += "; dimension tree: modes 0+1 in one pass over X (eb_exec_run_pair), mode 2 " \
+                 "separately — same outputs, 2/3 of the DMMA flops"
     use_nccl = world > 1 or args.transport == "nccl"
     nccl_id = None
     if world > 1:
@@ -375,9 +386,11 @@ def main():
             ins[0] = inputs[0][0]
             ex.share_input(0, execs[0], 0)
             shared = True
+            if dimtree and mi == 1:  # mode 1 also takes mode 0's C blocks (same tensor)
+                ex.share_input(2, execs[0], 2)
         elif mi > 0:
             ins = build(pinned=(world == 1))
-        ex.stage([None] + ins[1:] if shared else ins)
+        ex.stage(_stage_list(ins, shared, dimtree and mi == 1))
         execs.append(ex)
         inputs.append(ins)
         x_shared.append(shared)
@@ -387,6 +400,11 @@ def main():
     torch.cuda.synchronize()
 
     def step():
+        if dimtree:
+            if not execs[0].run_pair(execs[1]):
+                raise RuntimeError("dimension-tree pair did not qualify")
+            execs[2].run()
+            return
         for ex in execs:
             ex.run()
 
@@ -428,6 +446,13 @@ def main():
     ms_step = ms / args.steps
     value = flops_tree / (ms_step * 1e-3) / 1e9
 
+    # C2 with the reference's per-mode schedules: also time the same sweep with
+    # the dimension tree (modes 0+1 from one pass over X), reported beside the
+    # headline (which stays on the reference's decomposition).
+    alt = None
+    if args.config == "C2" and not dimtree:
+        alt = _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree)
+
     # e2e through the C ABI with host buffers.
     e2e = None
     if not args.no_e2e:
@@ -435,7 +460,8 @@ def main():
         h2d = 0
         for ins, ex_, sh in zip(inputs, execs, x_shared):
             # bytes this rank copies: its blocks of every operand it stages
-            h2d += _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh)
+            h2d += _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh,
+                                 skip2=dimtree and ex_ is execs[1])
         d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
         reps = max(1, min(args.steps, 3))
         if world > 1:
@@ -443,9 +469,10 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(reps):
-            for ins, ex_, out, sh in zip(inputs, execs, outs, x_shared):
-                ex_.stage([None] + list(ins[1:]) if sh else ins)
-                ex_.run()
+            for mi_, (ins, ex_, sh) in enumerate(zip(inputs, execs, x_shared)):
+                ex_.stage(_stage_list(ins, sh, dimtree and mi_ == 1))
+            step()
+            for ex_, out in zip(execs, outs):
                 ex_.gather(out)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / reps
@@ -470,8 +497,10 @@ def main():
     # over their CUDA-event time.
     kern_ms = kms.value / max(kn.value, 1)
     launches_per_step = max(kn.value // max(args.steps, 1), 1)
-    per_launch_flops = flops_tree / P / launches_per_step
-    achieved = (flops_tree / P) / (kms.value / args.steps * 1e-3) / 1e12
+    # executed DMMA flops: the dimension tree contracts X twice per sweep, not 3x
+    kflops = flops_tree * (2.0 / 3.0 if dimtree else 1.0)
+    per_launch_flops = kflops / P / launches_per_step
+    achieved = (kflops / P) / (kms.value / args.steps * 1e-3) / 1e12
     peaks = _load_peaks()
     traffic = _traffic(args.config)
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -481,7 +510,8 @@ def main():
                            "(MEASURED_PEAKS.json has no FP64 figure)",
             "kernel_ms_per_launch": kern_ms, "kernel_launches_timed": kn.value,
             "kernel_share_of_step": kms.value / max(ms, 1e-9),
-            "hbm_achieved_gbs": _x_bytes(modes, P) / (kms.value / args.steps * 1e-3) / 1e9,
+            "hbm_achieved_gbs": _x_bytes(modes, P) * (2.0 / 3.0 if dimtree else 1.0)
+                                / (kms.value / args.steps * 1e-3) / 1e9,
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
             "algorithmic_flops_per_launch": per_launch_flops,
             "launches_per_step": launches_per_step}
@@ -497,6 +527,7 @@ def main():
                    "l2": "inputs larger than L2 (X is 8.6 GB vs 126 MB L2), no flush needed"},
         "roofline": roof,
         "e2e": e2e,
+        **({"sweep_dimtree": alt} if alt else {}),
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -509,6 +540,49 @@ def main():
     return 0
 
 
+def _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree):
+    """Device time of the C2 sweep as ONE eb_exec_run_pair (mode 0 + mode 1,
+    T = X x_k C contracted once) plus the mode-2 executor, on the same staged
+    X / factors; a fourth executor for mode 1 shares X and C from mode 0."""
+    import torch
+    import torch.distributed as dist
+    ex0, ex1, ex2 = execs
+    m1 = eb.Executor(ex1.einsum, ex1.extents, stream=stream.cuda_stream, like=ex0)
+    m1.share_input(0, ex0, 0)
+    m1.share_input(2, ex0, 2)
+    m1.stage([None, inputs[1][1], None])
+
+    def step():
+        if not ex0.run_pair(m1):
+            raise RuntimeError("dimension-tree pair did not qualify")
+        ex2.run()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    return {"value": flops_tree / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "ms_per_step": ms_step,
+            "executed_dmma_tflops": flops_tree * 2 / 3 / (ms_step * 1e-3) / 1e12,
+            "frac_of_fp64_peak": flops_tree * 2 / 3 / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+            "note": "same three outputs; modes 0 and 1 share one contraction of X with C "
+                    "(2/3 of the per-mode DMMA flops); value counts the reference tree flops"}
+
+
 def _x_bytes(modes, P):
     tot = 0
     for e, ext, _ in modes:
@@ -517,9 +591,21 @@ def _x_bytes(modes, P):
     return tot
 
 
-def _staged_bytes(ex, ins, P, rank, eb, skip0=False):
+def _stage_list(ins, x_shared, c_shared):
+    """Host operands to stage: None for the ones aliased from executor 0."""
+    out = list(ins)
+    if x_shared:
+        out[0] = None
+    if c_shared:
+        out[2] = None
+    return out
+
+
+def _staged_bytes(ex, ins, P, rank, eb, skip0=False, skip2=False):
     if skip0:
         ins = [np.empty(0)] + list(ins[1:])
+    if skip2:
+        ins = list(ins[:2]) + [np.empty(0)] + list(ins[3:])
     if P == 1:
         return sum(a.nbytes for a in ins)
     # Blocks of this rank: every operand is split over the grid dims it spans

@@ -78,6 +78,18 @@ size_t eb_contract_workspace(const eb_contract_desc* d);
 int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* Dimension-tree pair (CP-ALS sweep, order 3): one pass over X computes the
+ * mode-0 MTTKRP (d: EB_ROW, EB_REDUCE, P = 1, one `mid` factor B, U = C) and
+ * the mode-1 MTTKRP  out1[j][r] = sum_{i,k} X[i,j,k] A[i,r] C[k,r]:
+ * T[i][j] = X[i][j][:] C is contracted once on DMMA and folded into
+ * out[i] (x B[j]) and out1[j] (x A[i]) — 2R flops per X element for two
+ * modes instead of 4R.  Needs M >= 128, R <= 64, L even.  The reference
+ * runs each mode as its own einsum (two run() calls); the outputs are the
+ * same up to FP64 summation order. */
+size_t eb_mttkrp2_workspace(const eb_contract_desc* d);
+int eb_mttkrp2(const eb_contract_desc* d, const double* A, int64_t lda, double* out1,
+               void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fused TTM pair: the two TTM steps of one fused term with the intermediate
  * kept on chip (TTMc-O5 terms [t0,t1] and [t2,out]; replaces two
  * local_contract calls, proj/src/executor.cpp:220-235):
@@ -161,6 +173,13 @@ int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
 int eb_exec_share_input(eb_exec* dst, int k_dst, eb_exec* src, int k_src);
 /* all terms: local contractions + reductions + redistributions, device only */
 int eb_exec_run(eb_exec* h);
+/* CP sweep dimension tree: run `mode0` (ijk,ja,ka->ia) and `mode1`
+ * (ijk,ia,ka->ja, X and the k factor shared from mode0 with
+ * eb_exec_share_input, same grid, same stream) in one pass over X with
+ * eb_mttkrp2, each output reduced over its own reference group.  *fused = 1
+ * when the pair ran fused, 0 when it did not qualify and both executors were
+ * run separately (same results). */
+int eb_exec_run_pair(eb_exec* mode0, eb_exec* mode1, int* fused);
 /* gather canonical output blocks to host (virtual mode, or rank 0) */
 int eb_exec_gather(eb_exec* h, double* host_out);
 int64_t eb_exec_output_elems(eb_exec* h);

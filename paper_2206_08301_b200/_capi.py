@@ -54,11 +54,11 @@ EXPORTS = [
     "einplan_version", "einplan_status_name", "einplan_last_error", "einplan_free",
     "einplan_session_create", "einplan_session_destroy", "einplan_bound_json",
     "einplan_plan_json", "einplan_run_json", "einplan_bench_json",
-    "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_ttm2",
+    "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_mttkrp2_workspace", "eb_mttkrp2", "eb_ttm2",
     "eb_step_generic",
     "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
-    "eb_exec_share_input", "eb_exec_run", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
+    "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
     "eb_exec_report_json", "eb_launch_count", "eb_timer_enable", "eb_timer_collect",
 ]
 
@@ -106,6 +106,10 @@ def lib():
         _sig(L, "eb_contract", ctypes.c_int,
              [ctypes.POINTER(ContractDesc), _vp, ctypes.c_size_t, _vp])
         _sig(L, "eb_ttm2", ctypes.c_int, [ctypes.POINTER(Ttm2Desc), _vp])
+        _sig(L, "eb_mttkrp2_workspace", ctypes.c_size_t, [ctypes.POINTER(ContractDesc)])
+        _sig(L, "eb_mttkrp2", ctypes.c_int,
+             [ctypes.POINTER(ContractDesc), _vp, _i64, _vp, _vp, ctypes.c_size_t, _vp])
+        _sig(L, "eb_exec_run_pair", ctypes.c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_int)])
         _sig(L, "eb_random_fill_host", None, [_dp, _i64, ctypes.c_uint64, _i64])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,

@@ -461,6 +461,18 @@ int eb_exec_run(eb_exec* h) {
   return exec_guard([&] { h->exec->execute(); });
 }
 
+int eb_exec_run_pair(eb_exec* mode0, eb_exec* mode1, int* fused) {
+  return exec_guard([&] {
+    if (!mode0 || !mode1) throw eb::InvalidError("eb_exec_run_pair: null handle");
+    const bool ok = mode0->exec->execute_pair(*mode1->exec);
+    if (!ok) {
+      mode0->exec->execute();
+      mode1->exec->execute();
+    }
+    if (fused) *fused = ok ? 1 : 0;
+  });
+}
+
 int eb_exec_gather(eb_exec* h, double* host_out) {
   return exec_guard([&] { h->exec->gather(host_out); });
 }

@@ -792,6 +792,102 @@ void ScheduleExecutor::execute() {
   }
 }
 
+bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
+  if (!staged_ || !m1.staged_) fail(errc::invalid_argument, "execute_pair: inputs not staged");
+  if (pipe_.schedule.terms.size() != 1 || m1.pipe_.schedule.terms.size() != 1) return false;
+  if (pipe_.schedule.procs != m1.pipe_.schedule.procs || owned_ != m1.owned_) return false;
+  if (m1.stream_ != stream_) return false;  // one stream orders the kernel and both reductions
+  const TermPlan& t0 = pipe_.schedule.terms[0];
+  const TermPlan& t1 = m1.pipe_.schedule.terms[0];
+  const MttkrpMatch a = match_mttkrp(t0.statement), b = match_mttkrp(t1.statement);
+  if (!a.ok || !b.ok || a.x_idx.size() != 3 || a.x_idx != b.x_idx || a.out_mode != 0 ||
+      b.out_mode != 1 || a.rank_sym != b.rank_sym)
+    return false;
+  // same grid over the same iteration dims: identical X / factor blocks per rank
+  if (t0.grid.order != t1.grid.order || t0.grid.dims != t1.grid.dims || t0.blocks != t1.blocks)
+    return false;
+  const auto& in0 = inputs_;
+  const auto& in1 = m1.inputs_;
+  auto blocks_of = [](const std::map<std::pair<int, std::string>, std::vector<DevBlock>>& m,
+                      const std::string& name) -> const std::vector<DevBlock>* {
+    const auto it = m.find({0, name});
+    return it == m.end() ? nullptr : &it->second;
+  };
+  const auto* x0 = blocks_of(in0, a.x_name);
+  const auto* x1 = blocks_of(in1, b.x_name);
+  const auto* c0 = blocks_of(in0, a.factor_of[2]);
+  const auto* c1 = blocks_of(in1, b.factor_of[2]);
+  const auto* bf = blocks_of(in0, a.factor_of[1]);
+  const auto* af = blocks_of(in1, b.factor_of[0]);
+  if (!x0 || !x1 || !c0 || !c1 || !bf || !af) return false;
+  for (std::int64_t r : owned_) {  // X and C must be the very same device blocks
+    const auto i = static_cast<std::size_t>(r);
+    if ((*x0)[i].ptr != (*x1)[i].ptr || (*c0)[i].ptr != (*c1)[i].ptr) return false;
+  }
+  // kernel preconditions, per owned rank
+  std::vector<eb_contract_desc> descs;
+  for (std::int64_t r : owned_) {
+    const auto i = static_cast<std::size_t>(r);
+    eb_contract_desc d;
+    std::memset(&d, 0, sizeof(d));
+    d.variant = EB_ROW;
+    d.mode = EB_REDUCE;
+    d.P = 1;
+    d.M = local_len(t0, a.x_idx[0], r);
+    d.Q = local_len(t0, a.x_idx[1], r);
+    d.L = local_len(t0, a.x_idx[2], r);
+    d.R = local_len(t0, a.rank_sym, r);
+    d.X = (*x0)[i].ptr;
+    d.U = (*c0)[i].ptr;
+    d.ldu = (*c0)[i].shape[1];
+    d.n_mid = 1;
+    d.mid[0].ptr = (*bf)[i].ptr;
+    d.mid[0].extent = (*bf)[i].shape[0];
+    d.mid[0].ld = (*bf)[i].shape[1];
+    d.out = (*x0)[i].ptr;  // placeholder for the shape query (set per launch below)
+    if (d.L % 2 || eb_mttkrp2_workspace(&d) == 0) return false;
+    descs.push_back(d);
+  }
+
+  for (ScheduleExecutor* e : {this, &m1}) {
+    e->run_arena_.release(e->stream_);
+    e->store_.clear();
+    e->comm_ = CommStats{};
+    e->comm_.per_rank_sent.assign(static_cast<std::size_t>(pipe_.schedule.procs), 0);
+    e->launches_fused_ = e->launches_ttm_ = e->launches_generic_ = 0;
+  }
+  const std::int64_t procs = pipe_.schedule.procs;
+  std::vector<DevBlock> out0(static_cast<std::size_t>(procs)), out1(static_cast<std::size_t>(procs));
+  std::size_t k = 0;
+  for (std::int64_t r : owned_) {
+    eb_contract_desc& d = descs[k++];
+    const auto i = static_cast<std::size_t>(r);
+    out0[i] = new_block(t0, t0.placement_of(t0.statement.output).indices, r, false);
+    out1[i] = m1.new_block(t1, t1.placement_of(t1.statement.output).indices, r, false);
+    d.out = out0[i].ptr;
+    const std::size_t wb = eb_mttkrp2_workspace(&d);
+    eb_ok(eb_mttkrp2(&d, (*af)[i].ptr, (*af)[i].shape[1], out1[i].ptr, workspace(wb), wb, stream_),
+          "eb_mttkrp2 (dimension-tree pair)");
+    ++launches_fused_;
+  }
+  struct Side {
+    ScheduleExecutor* e;
+    const TermPlan* t;
+    std::vector<DevBlock>* out;
+  };
+  for (const Side& sd : {Side{this, &t0, &out0}, Side{&m1, &t1, &out1}}) {
+    const TensorPlacement& place = sd.t->placement_of(sd.t->statement.output);
+    const std::int64_t v = sd.e->transport_->allreduce(place, sd.t->reduction, *sd.out,
+                                                       sd.e->comm_.per_rank_sent, sd.e->stream_);
+    if (sd.t->reduction.depth > 1) {
+      sd.e->comm_.events.push_back({"allreduce", sd.t->index, sd.t->statement.output, v});
+      sd.e->comm_.allreduce_volume += v;
+    }
+    sd.e->store_[{sd.t->index, sd.t->statement.output}] = std::move(*sd.out);
+  }
+  return true;
+}
+
 std::vector<std::int64_t> ScheduleExecutor::output_shape() const {
   return pipe_.spec.shape_of(pipe_.spec.output);
 }

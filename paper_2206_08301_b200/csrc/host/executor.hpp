@@ -107,6 +107,13 @@ class ScheduleExecutor {
   void share_input(int k, const ScheduleExecutor& src, int k_src);
   // All terms: local contractions, reductions, redistributions (device only).
   void execute();
+  // CP-sweep dimension tree: this executor (order-3 MTTKRP mode 0) and `mode1`
+  // (mode 1 over the same X and mode-2 factor, both shared from this one)
+  // in ONE pass over X — T = X x_k C is contracted once and folded into both
+  // outputs (eb_mttkrp2); each output is then reduced over its own reference
+  // reduction group.  Returns false (nothing run) when the pair does not
+  // qualify; the caller then runs both executors separately.
+  bool execute_pair(ScheduleExecutor& mode1);
   // Canonical output blocks to host (virtual, or rank 0 over NCCL).
   void gather(double* host_out);
   void verify(const std::vector<const double*>& global_inputs, const double* host_out,

@@ -66,6 +66,11 @@ struct ContractParams {
   FacList pre, mid;
   double* out;     // BATCHED: [P][M][ldo] ; REDUCE: partial slots
   int64_t ldo;
+  // TWO (dimension-tree second output, order-3 mode 0 + mode 1 in one pass):
+  // out2[mt][o][h][NP] += sum over the tile's rows m of A[m][c] * T[m][o][c]
+  const double* a2;  // factor of the row mode, row-major [M][lda2]
+  int64_t lda2;
+  double* out2;      // h = 0: the CTA that starts outer index o, 1: the one finishing it
 };
 
 __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col) {
@@ -185,6 +190,45 @@ __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const Co
     }
 }
 
+// TWO: outer index o is complete in this CTA — each warp scales its T rows by
+// A[row] and sums them (shuffles over the 8 row groups of a fragment), the NWM
+// warp sums meet in shared memory (double-buffered by emit parity), and warp 0
+// adds them in fixed order into slot (mt, o, h), h = 0 for the CTA that starts
+// o and 1 for the one that finishes it.
+template <int MI, int NT, int NWM, int MT, int WM>
+__device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
+                                         double (&red2)[2][NWM][NT * 8], const ContractParams& prm,
+                                         int64_t mt, int64_t o, int64_t o_kc0, int n_emit, int wm,
+                                         int g, int l, int lane) {
+  const int par = n_emit & 1;
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double x = 0.0;
+      const int c = prm.col0 + j * 8 + 2 * l + e;
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int64_t row = mt * MT + wm * WM + i * 8 + g;  // A[row][c]: L1-resident, once per o
+        const double av = (row < prm.M && c < prm.R) ? __ldg(prm.a2 + row * prm.lda2 + c) : 0.0;
+        x = fma(av, acc[i][j][e], x);
+      }
+#pragma unroll
+      for (int sh = 4; sh < 32; sh <<= 1) x += __shfl_xor_sync(0xffffffffu, x, sh);
+      if (g == 0) red2[par][wm][j * 8 + 2 * l + e] = x;
+    }
+  asm volatile("bar.sync 1, %0;" ::"n"(NWM * 32) : "memory");
+  if (wm == 0) {
+    double* dst = prm.out2 + ((mt * prm.O + o) * 2 + (o_kc0 > 0 ? 1 : 0)) * (NT * 8);
+    for (int c = lane; c < NT * 8; c += 32) {
+      double x = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWM; ++w) x += red2[par][w][c];
+      dst[c] = x;
+    }
+  }
+}
+
 // Warp roles:
 //   warp NCW       producer: lane 0 fills the stage ring with TMA boxes of X
 //                  and U; all 32 lanes write the stage's Khatri-Rao row
@@ -200,7 +244,7 @@ __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const Co
 // then M += KRP[o] (.) T once per outer index — the Khatri-Rao product is a
 // per-column scale of T and is never formed.  One partial per k-split group.
 // BATCHED (TTM) requires KS == 1 and writes each (row tile, o) unit once.
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false>
 __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
@@ -382,6 +426,15 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   int seg = -1;
   uint32_t it = 0;
 
+  // TWO: the second output.  When an outer index o is complete in this CTA,
+  // each warp scales its T rows by A[row] and sums them (shuffles over the 8
+  // row groups of a fragment), the NWM warp sums meet in shared memory, and
+  // warp 0 adds them in fixed order into slot (mt, o, h).
+  static_assert(!TWO || (!COL && !BATCHED && KS == 1 && OS == 1), "TWO: ROW REDUCE, KS = OS = 1");
+  __shared__ double red2[TWO ? 2 : 1][TWO ? NWM : 1][TWO ? NT * 8 : 1];
+  int64_t o_kc0 = 0;  // k chunk at which this CTA entered cur_o
+  int n_emit = 0;
+
   Cursor cur;
   cur.seek(i0, BATCHED, prm);
   for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
@@ -389,13 +442,19 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     const int64_t kc_begin = cur.kc;
     const int64_t kc_end = BATCHED ? prm.KC : kc_begin + 1;
     if constexpr (!BATCHED) if (o != cur_o || mt != cur_mt) {
-      if (cur_o >= 0) fold_krp<MI, NT>(acc, macc, krow);
+      if (cur_o >= 0) {
+        if constexpr (TWO)
+          emit_two<MI, NT, NWM, MT, WM>(acc, red2, prm, cur_mt, cur_o, o_kc0, n_emit++, wm, g, l,
+                                        lane);
+        fold_krp<MI, NT>(acc, macc, krow);
+      }
       if (mt != cur_mt) {
         if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
         ++seg;
         cur_mt = mt;
       }
       cur_o = o;
+      o_kc0 = kc_begin;
       // the new outer index's KRP row, from the first stage that carries it
       const int st = it % S;
       mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
@@ -472,6 +531,8 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   }
   if constexpr (!BATCHED) {
     if (cur_mt >= 0) {
+      if constexpr (TWO)
+        emit_two<MI, NT, NWM, MT, WM>(acc, red2, prm, cur_mt, cur_o, o_kc0, n_emit++, wm, g, l, lane);
       fold_krp<MI, NT>(acc, macc, krow);
       flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
     }
@@ -533,6 +594,23 @@ __global__ void __launch_bounds__(kReduceGroups * 64)
     for (int g2 = 0; g2 < kReduceGroups; ++g2) s += part[g2][n];
     out[m * ldo + col0 + n] = s;
   }
+}
+
+// TWO finish: out1[q][col0 + n] = sum over row tiles (ascending) and the two
+// CTA halves of every outer index (fixed order).
+__global__ void reduce_two_kernel(const double* __restrict__ slots, double* __restrict__ out1,
+                                  int64_t Q, int64_t mtiles, int R, int col0, int64_t ldo,
+                                  int NP) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Q * NP) return;
+  const int64_t q = idx / NP;
+  const int n = (int)(idx % NP);
+  if (col0 + n >= R) return;
+  double x = 0.0;
+  for (int64_t t = 0; t < mtiles; ++t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) x += slots[((t * Q + q) * 2 + h) * NP + n];
+  out1[q * ldo + col0 + n] = x;
 }
 
 // Uᵀ staging for the ROW variant (TMA needs k innermost): ut[n][l] = u[l][col0+n].
@@ -663,11 +741,11 @@ Plan plan_of(const eb_contract_desc* d) {
   return p;
 }
 
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
   using T = Tile<COL, NWM * WM, NT, KD, OS>;
-  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO>;
   static bool attr = false;
   if (!attr) {
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
@@ -800,9 +878,128 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   }
 }
 
+// Order-3 mode-0 MTTKRP that also emits mode 1 from the same pass
+// (dimension tree: T[i][j] = X[i][j][:] C is contracted once and folded with
+// B[j] into out0[i] and with A[i] into out1[j]).
+void check_two(const eb_contract_desc* d, const Plan& p) {
+  if (p.col || p.batched || p.nwm != 8 || p.ks != 1 || p.os != 1 || p.chunks != 1 || d->P != 1 ||
+      d->n_pre != 0 || d->n_mid != 1)
+    throw InvalidError("eb_mttkrp2: needs an order-3 mode-0 ROW REDUCE term with M >= 128, R <= 64");
+}
+
+size_t two_slot_bytes(const Plan& p) {
+  return ((size_t)p.mtiles * p.O * 2 * (p.nt * 8) * sizeof(double) + 255) / 256 * 256;
+}
+
+Plan two_plan(const eb_contract_desc* d) {
+  Plan p = plan_of(d);
+  check_two(d, p);
+  // every outer index may span at most two CTAs (slot h = 0 / 1)
+  if (p.items / p.G < p.KC) {
+    p.G = (int)std::max<int64_t>(1, p.items / p.KC);
+    const int64_t per_tile = p.O * p.KC;
+    int segmax = 1;
+    for (int c = 0; c < p.G; ++c) {
+      const int64_t c0 = (int64_t)c * p.items / p.G, c1 = (int64_t)(c + 1) * p.items / p.G;
+      if (c1 > c0) segmax = std::max<int>(segmax, (int)((c1 - 1) / per_tile - c0 / per_tile + 1));
+    }
+    p.segmax = segmax;
+    p.ws_bytes = ((size_t)p.G * segmax * p.mt * (p.nt * 8) * sizeof(double) + 255) / 256 * 256;
+  }
+  return p;
+}
+
+void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, double* out1, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  check_device();
+  const Plan p = two_plan(d);
+  if (!a || !out1 || lda < d->R) throw InvalidError("eb_mttkrp2: bad second-output factor / output");
+  const size_t slot_b = two_slot_bytes(p);
+  if (ws_bytes < p.u_bytes + p.ws_bytes + slot_b) throw InvalidError("eb_mttkrp2: workspace too small");
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  double* ubuf = reinterpret_cast<double*>(wsb);
+  double* part = reinterpret_cast<double*>(wsb + p.u_bytes);
+  double* slots = reinterpret_cast<double*>(wsb + p.u_bytes + p.ws_bytes);
+  EB_CUDA(cudaMemsetAsync(slots, 0, slot_b, st));
+
+  ContractParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.M = d->M;
+  prm.Q = d->Q;
+  prm.O = p.O;
+  prm.KC = p.KC;
+  prm.items = p.items;
+  prm.G = p.G;
+  prm.segmax = p.segmax;
+  prm.R = (int)d->R;
+  prm.pre = to_list(0, d->pre);
+  prm.mid = to_list(d->n_mid, d->mid);
+  prm.a2 = a;
+  prm.lda2 = lda;
+  prm.out2 = slots;
+  const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
+  const int nt = p.nt;
+  const int64_t lp = (d->L + 1) / 2 * 2;
+  const int64_t n = (int64_t)d->R * d->L;
+  transpose_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->L, (int)d->R, 0,
+                                                                   ubuf, lp);
+  EB_CUDA(cudaGetLastError());
+  count_launch();
+  CUtensorMap umap, xmap;
+  {
+    const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)d->R};
+    const uint64_t str[1] = {(uint64_t)lp * 8};
+    const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
+    umap = make_map(ubuf, 2, dims, str, box);
+  }
+  {
+    const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->M, (uint64_t)d->Q, 1};
+    const uint64_t str[3] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8,
+                             (uint64_t)(d->M * d->Q * d->L) * 8};
+    const uint32_t box[4] = {16, (uint32_t)p.mt, 1, 1};
+    xmap = make_map(d->X, 4, dims, str, box);
+  }
+  prm.out = part;
+  prm.ldo = d->R;
+  switch (nt) {
+#define EB_TWO_CASE(N) \
+  case N: launch_t<false, false, 8, 16, 1, 32, 1, N, true>(xmap, umap, prm, st); break;
+    EB_TWO_CASE(1) EB_TWO_CASE(2) EB_TWO_CASE(3) EB_TWO_CASE(4)
+    EB_TWO_CASE(5) EB_TWO_CASE(6) EB_TWO_CASE(7) EB_TWO_CASE(8)
+#undef EB_TWO_CASE
+    default: throw InvalidError("eb_mttkrp2: unsupported column tile count");
+  }
+  const int np = nt * 8;
+  reduce_partials_kernel<<<(unsigned)d->M, kReduceGroups * 64, 0, st>>>(
+      part, d->out, d->M, (int)d->R, 0, d->R, np, p.mt, 1, p.O * p.KC, p.items, p.G, p.segmax);
+  EB_CUDA(cudaGetLastError());
+  count_launch();
+  reduce_two_kernel<<<(unsigned)cdiv(d->Q * np, 256), 256, 0, st>>>(slots, out1, d->Q, p.mtiles,
+                                                                    (int)d->R, 0, d->R, np);
+  EB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 }  // namespace
 
 }  // namespace eb
+
+extern "C" size_t eb_mttkrp2_workspace(const eb_contract_desc* d) {
+  try {
+    const eb::Plan p = eb::two_plan(d);
+    return p.u_bytes + p.ws_bytes + eb::two_slot_bytes(p);
+  } catch (const std::exception& e) {
+    eb::set_error(e.what());
+    return 0;
+  }
+}
+
+extern "C" int eb_mttkrp2(const eb_contract_desc* d, const double* a, int64_t lda, double* out1,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  return eb::guard([&] {
+    eb::run_contract2(d, a, lda, out1, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
 
 extern "C" size_t eb_contract_workspace(const eb_contract_desc* d) {
   try {

@@ -174,6 +174,94 @@ def test_ttmc_o5_fused_terms(eb, P, monkeypatch):
     check(ex.gather(), want)
 
 
+MTTKRP2_SHAPES = [(130, 20, 34, 32), (256, 64, 64, 24), (128, 9, 2, 8), (300, 40, 18, 64),
+                  (257, 3, 6, 8), (128, 1, 2, 1), (512, 33, 130, 17)]
+
+
+@pytest.mark.parametrize("I,J,K,R", MTTKRP2_SHAPES)
+def test_mttkrp2_dimension_tree_pair(eb, I, J, K, R):
+    """eb_mttkrp2: one pass over X gives the mode-0 and the mode-1 MTTKRP
+    (T = X x_k C folded with B and with A), each equal to the oracle's own
+    naive_evaluate of that mode's einsum."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    ext = dict(i=I, j=J, k=K, a=R)
+    X = oracle.random_tensor((I, J, K), 0)
+    A, B, Cf = (oracle.random_tensor((n, R), s) for n, s in ((I, 1), (J, 2), (K, 3)))
+    want0 = oracle.naive_evaluate("ijk,ja,ka->ia", ext, [X, B, Cf])
+    want1 = oracle.naive_evaluate("ijk,ia,ka->ja", ext, [X, A, Cf])
+    g = {n: torch.from_numpy(t).cuda() for n, t in (("X", X), ("A", A), ("B", B), ("C", Cf))}
+    out0 = torch.full((I, R), float("nan"), dtype=torch.float64, device="cuda")
+    out1 = torch.full((J, R), float("nan"), dtype=torch.float64, device="cuda")
+    d = C.ContractDesc()
+    d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_ROW, C.EB_REDUCE, 1, I, J, K, R
+    d.X, d.U, d.ldu = g["X"].data_ptr(), g["C"].data_ptr(), R
+    d.n_mid = 1
+    d.mid[0] = C.Factor(g["B"].data_ptr(), J, R)
+    d.out = out0.data_ptr()
+    L_ = C.lib()
+    wb = L_.eb_mttkrp2_workspace(ctypes.byref(d))
+    assert wb > 0, L_.eb_last_error()
+    ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    C.check(L_.eb_mttkrp2(ctypes.byref(d), ctypes.c_void_p(g["A"].data_ptr()), R,
+                          ctypes.c_void_p(out1.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wb,
+                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    check(out0.cpu().numpy(), want0)
+    check(out1.cpu().numpy(), want1)
+
+
+def test_mttkrp2_rejects_small_row_tiles(eb):
+    from paper_2206_08301_b200 import _capi as C
+    d = C.ContractDesc()
+    d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_ROW, C.EB_REDUCE, 1, 64, 8, 8, 8
+    d.X = d.U = d.out = 8
+    d.n_mid = 1
+    d.mid[0] = C.Factor(8, 8, 8)
+    assert C.lib().eb_mttkrp2_workspace(ctypes.byref(d)) == 0  # M < 128: not this kernel
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_exec_run_pair_cp_sweep(eb, P):
+    """eb_exec_run_pair on the reference schedules of modes 0 and 1 (same grid
+    at every P): fused on every rank, both outputs equal the
+    oracle, and the reduction volumes equal those of two separate runs."""
+    ext = dict(i=256, j=256, k=128, a=16)
+    es = ["ijk,ja,ka->ia", "ijk,ia,ka->ja"]
+    X = oracle.random_tensor((256, 256, 128), 0)
+    F = {c: oracle.random_tensor((ext[c], 16), s) for c, s in (("i", 1), ("j", 2), ("k", 3))}
+    ex0 = eb.Executor(es[0], ext, P)
+    ex0.stage([X, F["j"], F["k"]])
+    ex1 = eb.Executor(es[1], ext, P)
+    ex1.share_input(0, ex0, 0)
+    ex1.share_input(2, ex0, 2)
+    ex1.stage([None, F["i"], None])
+    assert ex0.run_pair(ex1)
+    got0, got1 = ex0.gather(), ex1.gather()
+    st0, st1 = ex0.stats(), ex1.stats()
+    check(got0, oracle.naive_evaluate(es[0], ext, [X, F["j"], F["k"]]))
+    check(got1, oracle.naive_evaluate(es[1], ext, [X, F["i"], F["k"]]))
+    assert st0["fused_launches"] == P and st1["fused_launches"] == 0
+    ex0.run()
+    ex1.run()
+    assert ex0.stats()["allreduce_volume"] == st0["allreduce_volume"]
+    assert ex1.stats()["allreduce_volume"] == st1["allreduce_volume"]
+    check(ex0.gather(), got0)
+    check(ex1.gather(), got1)
+
+
+def test_exec_run_pair_falls_back_when_not_shared(eb):
+    ext = dict(i=128, j=32, k=32, a=8)
+    X = oracle.random_tensor((128, 32, 32), 0)
+    F = {c: oracle.random_tensor((ext[c], 8), s) for c, s in (("i", 1), ("j", 2), ("k", 3))}
+    ex0 = eb.Executor("ijk,ja,ka->ia", ext, 1)
+    ex0.stage([X, F["j"], F["k"]])
+    ex1 = eb.Executor("ijk,ia,ka->ja", ext, 1)
+    ex1.stage([X, F["i"], F["k"]])  # own copy of X: not the same blocks
+    assert not ex0.run_pair(ex1)
+    check(ex1.gather(), oracle.naive_evaluate("ijk,ia,ka->ja", ext, [X, F["i"], F["k"]]))
+
+
 def test_contract_order5_all_krp_rows(eb):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
@@ -305,6 +393,25 @@ def test_c2_full_size(eb, mode):
     ex.stage(c2_inputs(mode, ext))
     ex.run()
     _against_golden(f"C2_m{mode}", ex.gather())
+
+
+def test_c2_full_size_dimension_tree(eb):
+    """The CP sweep with the dimension tree (bench.py --sweep dimtree): modes 0
+    and 1 from one pass over the 8.6 GB X must still match the reference's
+    own per-mode outputs (goldens)."""
+    c = CONFIGS["C2"]
+    ext = c["extents"](1)
+    e0, e1 = c["einsums"][0], c["einsums"][1]
+    ins0, ins1 = c2_inputs(0, ext), c2_inputs(1, ext)
+    ex0 = eb.Executor(e0, ext, 1)
+    ex0.stage(ins0)
+    ex1 = eb.Executor(e1, ext, 1)
+    ex1.share_input(0, ex0, 0)
+    ex1.share_input(2, ex0, 2)
+    ex1.stage([None, ins1[1], None])
+    assert ex0.run_pair(ex1)
+    _against_golden("C2_m0", ex0.gather())
+    _against_golden("C2_m1", ex1.gather())
 
 
 def test_c3_full_size(eb):

@@ -1,11 +1,23 @@
-"""Run one eb_contract configuration a few times (for ncu captures)."""
-import ctypes, sys
+"""Run eb_contract on a BASELINE term shape: a few launches (for ncu captures),
+or timed A/B variants with CUDA events.
+
+usage: python tools/prof_contract.py CFG [REPS] [ENV=VAL,... ...]
+  CFG in c1, c2m0, c2m1, c2m2, c3.  With variant args, the variants are run
+  round-robin (3 rounds) and the best ms / TFLOP/s of each is printed.
+"""
+import ctypes
+import json
+import os
+import sys
+
 import torch
-sys.path.insert(0, "/root/repo")
-from paper_2206_08301_b200 import _capi as C
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2206_08301_b200 import _capi as C  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2m0"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+variants = sys.argv[3:]
 dev = torch.device("cuda:0")
 
 
@@ -32,19 +44,52 @@ if cfg.startswith("c2"):
     d = {"c2m0": lambda: desc(C.EB_ROW, 1, 1024, 1024, 1024, 32, X, Cm, [], [B], out),
          "c2m1": lambda: desc(C.EB_ROW, 1024, 1024, 1, 1024, 32, X, Cm, [A], [], out),
          "c2m2": lambda: desc(C.EB_COL, 1024, 1024, 1024, 0, 32, X, B, [A], [], out)}[cfg]()
+    flops = 2.0 * 1024 ** 3 * 32
 elif cfg == "c1":
     X = r(512, 512, 512); B, Cm = r(512, 24), r(512, 24)
     out = torch.zeros(512, 24, dtype=torch.float64, device=dev)
     d = desc(C.EB_ROW, 1, 512, 512, 512, 24, X, Cm, [], [B], out)
+    flops = 2.0 * 512 ** 3 * 24
 elif cfg == "c3":
     X = r(64, 64, 64, 64, 64); F = [r(64, 24) for _ in range(4)]
     out = torch.zeros(64, 24, dtype=torch.float64, device=dev)
     d = desc(C.EB_ROW, 1, 64, 64 ** 3, 64, 24, X, F[3], [], F[:3], out)
+    flops = 2.0 * 64 ** 5 * 24
 L = C.lib()
 wsb = L.eb_contract_workspace(ctypes.byref(d))
 ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-for _ in range(reps):
+
+
+def launch():
     C.check(L.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wsb, st))
-torch.cuda.synchronize()
-print("done", cfg)
+
+
+if not variants:
+    for _ in range(reps):
+        launch()
+    torch.cuda.synchronize()
+    print("done", cfg)
+    sys.exit(0)
+
+res = {}
+for rnd in range(3):
+    for v in variants:
+        kv = [x.split("=") for x in v.split(",") if x]
+        for k, val in kv:
+            os.environ[k] = val
+        launch(); launch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            launch()
+        e1.record()
+        torch.cuda.synchronize()
+        res.setdefault(v, []).append(e0.elapsed_time(e1) / reps)
+        for k, _ in kv:
+            os.environ.pop(k, None)
+for v, ms in res.items():
+    print(json.dumps({"cfg": cfg, "variant": v, "ms_best": round(min(ms), 4),
+                      "ms_all": [round(x, 4) for x in ms],
+                      "TFLOPs": round(flops / min(ms) / 1e9, 2)}))
