@@ -62,6 +62,10 @@ st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def launch():
+    global ws, wsb
+    need = L.eb_contract_workspace(ctypes.byref(d))  # the tiling may depend on EB_* knobs
+    if need > wsb:
+        wsb, ws = need, torch.empty(need, dtype=torch.uint8, device=dev)
     C.check(L.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wsb, st))
 
 
