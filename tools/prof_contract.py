@@ -2,7 +2,7 @@
 or timed A/B variants with CUDA events.
 
 usage: python tools/prof_contract.py CFG [REPS] [ENV=VAL,... ...]
-  CFG in c1, c2m0, c2m1, c2m2, c3.  With variant args, the variants are run
+  CFG in c1, c2m0, c2m1, c2m2, c2pair (eb_mttkrp2: modes 0+1 in one pass), c3.  With variant args, the variants are run
   round-robin (3 rounds) and the best ms / TFLOP/s of each is printed.
 """
 import ctypes
@@ -41,7 +41,9 @@ r = lambda *s: torch.rand(*s, dtype=torch.float64, device=dev)
 if cfg.startswith("c2"):
     X = r(1024, 1024, 1024); A, B, Cm = r(1024, 32), r(1024, 32), r(1024, 32)
     out = torch.zeros(1024, 32, dtype=torch.float64, device=dev)
+    out1 = torch.zeros(1024, 32, dtype=torch.float64, device=dev)
     d = {"c2m0": lambda: desc(C.EB_ROW, 1, 1024, 1024, 1024, 32, X, Cm, [], [B], out),
+         "c2pair": lambda: desc(C.EB_ROW, 1, 1024, 1024, 1024, 32, X, Cm, [], [B], out),
          "c2m1": lambda: desc(C.EB_ROW, 1024, 1024, 1, 1024, 32, X, Cm, [A], [], out),
          "c2m2": lambda: desc(C.EB_COL, 1024, 1024, 1024, 0, 32, X, B, [A], [], out)}[cfg]()
     flops = 2.0 * 1024 ** 3 * 32
@@ -56,17 +58,23 @@ elif cfg == "c3":
     d = desc(C.EB_ROW, 1, 64, 64 ** 3, 64, 24, X, F[3], [], F[:3], out)
     flops = 2.0 * 64 ** 5 * 24
 L = C.lib()
-wsb = L.eb_contract_workspace(ctypes.byref(d))
+pair = cfg == "c2pair"
+wsfn = L.eb_mttkrp2_workspace if pair else L.eb_contract_workspace
+wsb = wsfn(ctypes.byref(d))
 ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def launch():
     global ws, wsb
-    need = L.eb_contract_workspace(ctypes.byref(d))  # the tiling may depend on EB_* knobs
+    need = wsfn(ctypes.byref(d))  # the tiling may depend on EB_* knobs
     if need > wsb:
         wsb, ws = need, torch.empty(need, dtype=torch.uint8, device=dev)
-    C.check(L.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wsb, st))
+    if pair:
+        C.check(L.eb_mttkrp2(ctypes.byref(d), ctypes.c_void_p(A.data_ptr()), 32,
+                             ctypes.c_void_p(out1.data_ptr()), ctypes.c_void_p(ws.data_ptr()), wsb, st))
+    else:
+        C.check(L.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wsb, st))
 
 
 if not variants:
