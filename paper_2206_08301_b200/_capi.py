@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libeinplan_b200.so")
+# EB_LIB_PATH: load another build of the library (A/B timing of two builds)
+LIB_PATH = os.environ.get("EB_LIB_PATH") or os.path.join(_HERE, "lib", "libeinplan_b200.so")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _vp = ctypes.c_void_p
