@@ -541,45 +541,50 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
 
 // Deterministic split-K finish: out[m][col0+n] = sum over the CTAs whose item
 // range touches row tile m / MT (ascending), and over their SPL partial slots
-// (k-split x outer-index groups).  One block per output row: thread (g, n)
-// sums every kGroups-th contribution of column n with batched independent
-// loads, then the kGroups partial sums are added in fixed order — the result
-// is bitwise reproducible and no FP64 atomics are used.
+// (k-split x outer-index groups).  One block per output row: the block first
+// resolves, once per contributing CTA, that CTA's partial-slot base (the
+// 64-bit divisions of the item split: one per CTA per block, shared in smem),
+// then thread (g, n) adds every kReduceGroups-th (CTA, slot) contribution of
+// column n with batched independent loads, and the group sums are combined
+// in fixed order — bitwise reproducible, no FP64 atomics.
 constexpr int kReduceGroups = 8;
+constexpr int kMaxCtas = 1024;
 
 __global__ void __launch_bounds__(kReduceGroups * 64)
     reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out, int64_t M,
-                           int R, int col0, int64_t ldo, int NP, int MT, int SPL,
-                           int64_t per_tile, int64_t items, int G, int segmax) {
+                            int R, int col0, int64_t ldo, int NP, int MT, int SPL,
+                            int64_t per_tile, int64_t items, int G, int segmax) {
+  __shared__ int64_t slot_base[kMaxCtas];
   __shared__ double part[kReduceGroups][64];
   const int64_t m = blockIdx.x;
   const int n = threadIdx.x % 64, grp = threadIdx.x / 64;
   const int64_t t = m / MT;
   const int64_t lo = t * per_tile, hi = lo + per_tile;
-  // CTAs c with [c*items/G, (c+1)*items/G) overlapping [lo, hi):
-  //   c >= ceil((lo+1)*G/items) - 1  and  c <= ceil(hi*G/items) - 1.
   const int64_t cmin = ((lo + 1) * G + items - 1) / items - 1;
   const int64_t cmax = (hi * G + items - 1) / items - 1;
   const int64_t cbeg = cmin < 0 ? 0 : cmin;
-  const int64_t cend = (cmax < G - 1 ? cmax : G - 1) + 1;
-  const int64_t total = (cend - cbeg) * SPL;
+  const int nc = (int)((cmax < G - 1 ? cmax : G - 1) + 1 - cbeg);
+  for (int j = threadIdx.x; j < nc; j += kReduceGroups * 64) {
+    const int64_t c = cbeg + j;
+    const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
+    slot_base[j] = (c1 <= lo || c0 >= hi || c1 <= c0) ? -1 : (c * segmax + (t - c0 / per_tile)) * SPL;
+  }
+  __syncthreads();
+  const int total = nc * SPL;
+  const int mr = (int)(m % MT);
   double acc = 0.0;
   if (n < NP) {
     constexpr int kBatch = 8;
-    for (int64_t b = grp; b < total; b += kReduceGroups * kBatch) {
+    for (int b = grp; b < total; b += kReduceGroups * kBatch) {
       double v[kBatch];
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
         v[u] = 0.0;
-        const int64_t e = b + (int64_t)u * kReduceGroups;
+        const int e = b + u * kReduceGroups;
         if (e < total) {
-          const int64_t c = cbeg + e / SPL;
-          const int k = (int)(e % SPL);
-          const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
-          if (!(c1 <= lo || c0 >= hi || c1 <= c0)) {
-            const int64_t sg = t - c0 / per_tile;
-            v[u] = ws[(((c * segmax + sg) * SPL + k) * MT + (m % MT)) * NP + n];
-          }
+          const int j = e / SPL, k = e - j * SPL;
+          const int64_t base = slot_base[j];
+          if (base >= 0) v[u] = ws[((base + k) * MT + mr) * NP + n];
         }
       }
 #pragma unroll
@@ -589,11 +594,21 @@ __global__ void __launch_bounds__(kReduceGroups * 64)
   part[grp][n] = acc;
   __syncthreads();
   if (grp == 0 && n < NP && col0 + n < R) {
-    double s = 0.0;
+    double x = 0.0;
 #pragma unroll
-    for (int g2 = 0; g2 < kReduceGroups; ++g2) s += part[g2][n];
-    out[m * ldo + col0 + n] = s;
+    for (int g2 = 0; g2 < kReduceGroups; ++g2) x += part[g2][n];
+    out[m * ldo + col0 + n] = x;
   }
+}
+
+void launch_reduce(const double* ws, double* out, int64_t M, int R, int col0, int64_t ldo, int NP,
+                   int MT, int SPL, int64_t per_tile, int64_t items, int G, int segmax,
+                   cudaStream_t st) {
+  if (G > kMaxCtas) throw InvalidError("eb_contract: too many CTAs for the partial reduction");
+  reduce_partials_kernel<<<(unsigned)M, kReduceGroups * 64, 0, st>>>(
+      ws, out, M, R, col0, ldo, NP, MT, SPL, per_tile, items, G, segmax);
+  EB_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 // TWO finish: out1[q][col0 + n] = sum over row tiles (ascending) and the two
@@ -869,11 +884,8 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     launch_variant(p, nt, xmap, umap, q, st);
     if (!p.batched) {
       const int np = nt * 8;
-      reduce_partials_kernel<<<(unsigned)d->M, kReduceGroups * 64, 0, st>>>(
-          part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks * p.os, p.O * p.KC, p.items, p.G,
-          p.segmax);
-      EB_CUDA(cudaGetLastError());
-      count_launch();
+      launch_reduce(part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks * p.os, p.O * p.KC,
+                    p.items, p.G, p.segmax, st);
     }
   }
 }
@@ -970,10 +982,8 @@ void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, doub
     default: throw InvalidError("eb_mttkrp2: unsupported column tile count");
   }
   const int np = nt * 8;
-  reduce_partials_kernel<<<(unsigned)d->M, kReduceGroups * 64, 0, st>>>(
-      part, d->out, d->M, (int)d->R, 0, d->R, np, p.mt, 1, p.O * p.KC, p.items, p.G, p.segmax);
-  EB_CUDA(cudaGetLastError());
-  count_launch();
+  launch_reduce(part, d->out, d->M, (int)d->R, 0, d->R, np, p.mt, 1, p.O * p.KC, p.items, p.G,
+                p.segmax, st);
   reduce_two_kernel<<<(unsigned)cdiv(d->Q * np, 256), 256, 0, st>>>(slots, out1, d->Q, p.mtiles,
                                                                     (int)d->R, 0, d->R, np);
   EB_CUDA(cudaGetLastError());
