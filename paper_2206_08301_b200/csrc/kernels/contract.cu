@@ -71,6 +71,9 @@ struct ContractParams {
   const double* a2;  // factor of the row mode, row-major [M][lda2]
   int64_t lda2;
   double* out2;      // h = 0: the CTA that starts outer index o, 1: the one finishing it
+  // one TMA box per operand per stage: the 16-wide column blocks are a tensor
+  // dimension of the maps (contiguous extent a multiple of 16)
+  int fused_tma;
 };
 
 __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col) {
@@ -128,7 +131,8 @@ struct Tile {
   static constexpr int kScaleBytes = ((OS * NT * 64) + 1023) / 1024 * 1024;  // OS KRP rows
   static constexpr int kStageBytes = kXBytes + kUBytes + kScaleBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static constexpr int kLastBytes = 16 * 1024;  // REDUCE: the KRP lane table of the last factor
+  static constexpr int kSmem = kStages * kStageBytes + kLastBytes + 1024;
   static_assert(kXBytes % 1024 == 0 && kUBytes % 1024 == 0, "swizzle atoms need 1 KB alignment");
   static_assert(kStages >= 2, "stage too large");
 };
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     }
     uint32_t it = 0;
     int64_t scale_g = -1;  // outer-index group whose KRP rows are in kv[]
+    int64_t t_o = -1, tp = 0, tq = 0;  // ROW: outer-index group -> (p, q), incremental
     // The stage's OS x NP Khatri-Rao values, spread over the 32 lanes: slot
     // u holds value v = lane + 32u = (outer index v / NP, column v % NP).
     constexpr int NP = NT * 8;
@@ -296,6 +301,34 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     double kv[VPL];
     KrpSlot slot[VPL];
     const bool has_krp = (COL ? 0 : prm.mid.n) + prm.pre.n > 0;
+    // Lane-per-column KRP path (NP <= 32, OS | ext of the last factor): the OS
+    // outer indices of a stage share one prefix product, so a lane produces
+    // its column's OS values as prefix x last[digit + s] — a handful of
+    // instructions per stage.  The producer shares its SM sub-partition with
+    // two DMMA-saturated consumer warps and gets an issue slot only every few
+    // tens of cycles, so its instruction count, not its memory latency, is
+    // what gates the ring (the general slot path below costs ~2.5k cycles
+    // per order-5 stage).  The last factor's column block sits in shared
+    // memory when it fits.
+    constexpr bool kLaneCol = NP <= 32 && !TWO;  // (TWO sits at the register cap)
+    const FacList& lastf = krp_last_list(prm, COL);
+    const int64_t fe = has_krp ? lastf.ext[lastf.n - 1] : 1;
+    const bool fast = kLaneCol && !BATCHED && has_krp && fe % OS == 0;
+    const int fcol = prm.col0 + lane;
+    const bool flane = lane < NP && fcol < prm.R;
+    double* last_s = reinterpret_cast<double*>(sbase + S * T::kStageBytes);
+    const bool fcached = fast && fe * NP * 8 <= T::kLastBytes;
+    if (fcached) {
+      for (int64_t x = lane; x < fe * NP; x += 32) {
+        const int c = prm.col0 + (int)(x % NP);
+        last_s[x] =
+            c < prm.R ? __ldg(lastf.ptr[lastf.n - 1] + (x / NP) * lastf.ld[lastf.n - 1] + c) : 0.0;
+      }
+      __syncwarp();
+    }
+    int64_t fd0 = 0, frest = -1;
+    double fprefix = 0.0;
+    double kvf[kLaneCol ? OS : 1];
     Cursor cur;
     cur.seek(i0, BATCHED, prm);
     for (int64_t item = i0; item < i1; ++item, cur.advance(BATCHED, prm)) {
@@ -314,13 +347,41 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
           const int k0 = (int)(kc * KD);
           const int64_t ob = o * OS;  // first outer index of the stage
           if (!COL) {
-            // X map dims {L, M, Q, P}: box {16, MT, OS, 1} -> smem [OS][MT][16]
-            const int p = (int)(ob / prm.Q), q = (int)(ob % prm.Q);
-#pragma unroll
-            for (int b = 0; b < KD / 16; ++b) {
-              tma_load_4d(xs + b * OS * MT * 128, &xmap, fb, k0 + 16 * b, (int)(mt * MT), q, p);
-              tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, 0);
+            // the producer shares an SMSP with DMMA-saturated warps and gets
+            // few issue slots: (p, q) advance incrementally (Q % OS == 0),
+            // no 64-bit division per stage
+            if (o != t_o) {
+              if (t_o >= 0 && o == t_o + 1) {
+                tq += OS;
+                if (tq >= prm.Q) {
+                  tq = 0;
+                  ++tp;
+                }
+              } else {
+                tp = ob / prm.Q;
+                tq = ob % prm.Q;
+              }
+              t_o = o;
             }
+            if (prm.fused_tma) {
+              // X dims {16, M, Q, L/16, P}: box {16, MT, OS, KD/16, 1} -> [b][OS][MT][16]
+              tma_load_5d(xs, &xmap, fb, 0, (int)(mt * MT), (int)tq, k0 / 16, (int)tp);
+              // Uᵀ dims {16, cols, L/16}: box {16, NP, KD/16} -> [b][NP][16]
+              tma_load_3d(us, &umap, fb, 0, 0, k0 / 16);
+            } else {
+              // X map dims {L, M, Q, P}: box {16, MT, OS, 1} -> smem [OS][MT][16]
+#pragma unroll
+              for (int b = 0; b < KD / 16; ++b) {
+                tma_load_4d(xs + b * OS * MT * 128, &xmap, fb, k0 + 16 * b, (int)(mt * MT),
+                            (int)tq, (int)tp);
+                tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, 0);
+              }
+            }
+          } else if (prm.fused_tma) {
+            // X dims {16, Q, P, M/16}: box {16, KD, OS, MT/16} -> [b][OS][KD][16]
+            tma_load_4d(xs, &xmap, fb, 0, k0, (int)ob, (int)(mt * MT) / 16);
+            // U dims {16, Q, pitch/16}: box {16, KD, NP/16} -> [b][KD][16]
+            tma_load_3d(us, &umap, fb, 0, k0, prm.col0 / 16);
           } else {
             // X map dims {M, Q, P}: box {16, KD, OS} -> smem [OS][KD][16]
 #pragma unroll
@@ -331,7 +392,39 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
               tma_load_2d(us + b * KD * 128, &umap, fb, prm.col0 + 16 * b, k0);
           }
         }
-        if (!BATCHED) {
+        if (!BATCHED && fast) {
+          if (o != scale_g) {
+            const bool next = scale_g >= 0 && o == scale_g + 1;
+            scale_g = o;
+            const int64_t rest0 = frest;
+            if (next) {
+              fd0 += OS;
+              if (fd0 >= fe) {
+                fd0 -= fe;
+                ++frest;
+              }
+            } else {
+              const int64_t ob = o * OS;
+              fd0 = ob % fe;
+              frest = ob / fe;
+            }
+            if (frest != rest0) fprefix = flane ? krp_prefix(prm, COL, frest, fcol) : 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < (kLaneCol ? OS : 1); ++s2)
+              kvf[s2] = !flane ? 0.0
+                        : fprefix * (fcached ? last_s[(fd0 + s2) * NP + lane]
+                                             : __ldg(lastf.ptr[lastf.n - 1] +
+                                                     (fd0 + s2) * lastf.ld[lastf.n - 1] + fcol));
+          }
+          double* sc = reinterpret_cast<double*>(sbase + st * T::kStageBytes + T::kXBytes +
+                                                 T::kUBytes);
+          if (lane < NP) {
+#pragma unroll
+            for (int s2 = 0; s2 < (kLaneCol ? OS : 1); ++s2) sc[s2 * NP + lane] = kvf[s2];
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(fb);  // second arrival: the KRP rows are in place
+        } else if (!BATCHED) {
           if (o != scale_g) {
             const bool next = scale_g >= 0 && o == scale_g + 1;
             scale_g = o;
@@ -747,7 +840,7 @@ Plan plan_of(const eb_contract_desc* d) {
     p.ws_bytes = (size_t)p.G * segmax * p.ks * p.os * p.mt * (p.nt * 8) * sizeof(double);
   }
   if (p.col) {
-    p.u_bytes = (size_t)d->Q * ((d->R + 1) / 2 * 2) * sizeof(double);
+    p.u_bytes = (size_t)d->Q * ((d->R + 15) / 16 * 16) * sizeof(double);
   } else {
     p.u_bytes = (size_t)p.nt * 8 * ((d->L + 1) / 2 * 2) * sizeof(double);
   }
@@ -828,9 +921,11 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   prm.mid = to_list(p.col ? 0 : d->n_mid, d->mid);
   const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
 
-  // COL stages the whole factor once (pitch = even R); ROW stages Uᵀ per
-  // 64-column chunk.
-  int64_t pitch = (d->R + 1) / 2 * 2;
+  // COL stages the whole factor once (pitch = R rounded up to 16, zero
+  // padded); ROW stages Uᵀ per 64-column chunk.
+  const int64_t pitch = (d->R + 15) / 16 * 16;
+  // one box per operand per stage when the contiguous extent tiles by 16
+  prm.fused_tma = (p.col ? d->M % 16 == 0 : d->L % 16 == 0) && !std::getenv("EB_NO_FUSED_TMA") ? 1 : 0;
   CUtensorMap umap_col;
   if (p.col) {
     const int64_t n = d->Q * pitch;
@@ -838,13 +933,32 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
                                                                  pitch);
     EB_CUDA(cudaGetLastError());
     count_launch();
-    const uint64_t dims[2] = {(uint64_t)d->R, (uint64_t)d->Q};
-    const uint64_t str[1] = {(uint64_t)pitch * 8};
-    const uint32_t box[2] = {16, (uint32_t)p.kd};
-    umap_col = make_map(ubuf, 2, dims, str, box);
+    if (prm.fused_tma) {
+      const uint64_t dims[3] = {16, (uint64_t)d->Q, (uint64_t)(pitch / 16)};
+      const uint64_t str[2] = {(uint64_t)pitch * 8, 128};
+      const uint32_t box[3] = {16, (uint32_t)p.kd, (uint32_t)((p.nt * 8 + 15) / 16)};
+      umap_col = make_map(ubuf, 3, dims, str, box);
+    } else {
+      const uint64_t dims[2] = {(uint64_t)d->R, (uint64_t)d->Q};
+      const uint64_t str[1] = {(uint64_t)pitch * 8};
+      const uint32_t box[2] = {16, (uint32_t)p.kd};
+      umap_col = make_map(ubuf, 2, dims, str, box);
+    }
   }
   CUtensorMap xmap;
-  if (!p.col) {
+  if (!p.col && prm.fused_tma) {
+    const uint64_t dims[5] = {16, (uint64_t)d->M, (uint64_t)d->Q, (uint64_t)(d->L / 16),
+                              (uint64_t)d->P};
+    const uint64_t str[4] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8, 128,
+                             (uint64_t)(d->M * d->Q * d->L) * 8};
+    const uint32_t box[5] = {16, (uint32_t)p.mt, (uint32_t)p.os, (uint32_t)(p.kd / 16), 1};
+    xmap = make_map(d->X, 5, dims, str, box);
+  } else if (p.col && prm.fused_tma) {
+    const uint64_t dims[4] = {16, (uint64_t)d->Q, (uint64_t)d->P, (uint64_t)(d->M / 16)};
+    const uint64_t str[3] = {(uint64_t)d->M * 8, (uint64_t)(d->Q * d->M) * 8, 128};
+    const uint32_t box[4] = {16, (uint32_t)p.kd, (uint32_t)p.os, (uint32_t)(p.mt / 16)};
+    xmap = make_map(d->X, 4, dims, str, box);
+  } else if (!p.col) {
     // dims {L, M, Q, P} (M before Q so one box holds OS outer indices of MT rows)
     const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->M, (uint64_t)d->Q, (uint64_t)d->P};
     const uint64_t str[3] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8,
@@ -871,10 +985,17 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
                                                                        ubuf, lp);
       EB_CUDA(cudaGetLastError());
       count_launch();
-      const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)cols};
-      const uint64_t str[1] = {(uint64_t)lp * 8};
-      const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
-      umap = make_map(ubuf, 2, dims, str, box);
+      if (prm.fused_tma) {
+        const uint64_t dims[3] = {16, (uint64_t)cols, (uint64_t)(d->L / 16)};
+        const uint64_t str[2] = {(uint64_t)lp * 8, 128};
+        const uint32_t box[3] = {16, (uint32_t)(nt * 8), (uint32_t)(p.kd / 16)};
+        umap = make_map(ubuf, 3, dims, str, box);
+      } else {
+        const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)cols};
+        const uint64_t str[1] = {(uint64_t)lp * 8};
+        const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
+        umap = make_map(ubuf, 2, dims, str, box);
+      }
     } else {
       umap = umap_col;
     }
@@ -958,13 +1079,22 @@ void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, doub
   EB_CUDA(cudaGetLastError());
   count_launch();
   CUtensorMap umap, xmap;
-  {
-    const uint64_t dims[2] = {(uint64_t)d->L, (uint64_t)d->R};
-    const uint64_t str[1] = {(uint64_t)lp * 8};
-    const uint32_t box[2] = {16, (uint32_t)(nt * 8)};
-    umap = make_map(ubuf, 2, dims, str, box);
-  }
-  {
+  prm.fused_tma = d->L % 16 == 0 && !std::getenv("EB_NO_FUSED_TMA") ? 1 : 0;
+  if (prm.fused_tma) {
+    const uint64_t udims[3] = {16, (uint64_t)d->R, (uint64_t)(d->L / 16)};
+    const uint64_t ustr[2] = {(uint64_t)lp * 8, 128};
+    const uint32_t ubox[3] = {16, (uint32_t)(nt * 8), (uint32_t)(p.kd / 16)};
+    umap = make_map(ubuf, 3, udims, ustr, ubox);
+    const uint64_t dims[5] = {16, (uint64_t)d->M, (uint64_t)d->Q, (uint64_t)(d->L / 16), 1};
+    const uint64_t str[4] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8, 128,
+                             (uint64_t)(d->M * d->Q * d->L) * 8};
+    const uint32_t box[5] = {16, (uint32_t)p.mt, 1, (uint32_t)(p.kd / 16), 1};
+    xmap = make_map(d->X, 5, dims, str, box);
+  } else {
+    const uint64_t udims[2] = {(uint64_t)d->L, (uint64_t)d->R};
+    const uint64_t ustr[1] = {(uint64_t)lp * 8};
+    const uint32_t ubox[2] = {16, (uint32_t)(nt * 8)};
+    umap = make_map(ubuf, 2, udims, ustr, ubox);
     const uint64_t dims[4] = {(uint64_t)d->L, (uint64_t)d->M, (uint64_t)d->Q, 1};
     const uint64_t str[3] = {(uint64_t)(d->Q * d->L) * 8, (uint64_t)d->L * 8,
                              (uint64_t)(d->M * d->Q * d->L) * 8};
