@@ -483,6 +483,13 @@ def main():
         e2e = {"value": flops_tree / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
                "host_buffers": "pinned" if world == 1 else "pageable"}
+        if world == 1:
+            # the e2e roofline: the same bytes through one plain pinned H2D copy
+            bw = _h2d_gbs(int(h2d))
+            if bw:
+                e2e["h2d_copy_gbs"] = bw
+                e2e["h2d_only_ms"] = h2d / (bw * 1e9) * 1e3
+                e2e["frac_of_h2d_bound"] = (h2d / (bw * 1e9)) / dt
 
     if rank != 0:
         if world > 1:
@@ -581,6 +588,29 @@ def _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree):
             "frac_of_fp64_peak": flops_tree * 2 / 3 / (ms_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
             "note": "same three outputs; modes 0 and 1 share one contraction of X with C "
                     "(2/3 of the per-mode DMMA flops); value counts the reference tree flops"}
+
+
+def _h2d_gbs(nbytes):
+    """Bandwidth of one pinned host -> device copy of `nbytes` (best of 3)."""
+    import torch
+    try:
+        n = max(nbytes // 8, 1)
+        h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        d = torch.empty(n, dtype=torch.float64, device="cuda")
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            d.copy_(h, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del h, d
+        torch.cuda.empty_cache()
+        return n * 8 / (best * 1e-3) / 1e9
+    except Exception:
+        return None
 
 
 def _x_bytes(modes, P):

@@ -293,6 +293,46 @@ def test_run_json_desk_kernels(eb, name, einsum, ext, P):
     check(got, want)
 
 
+def _random_case(rng):
+    """A random MTTKRP (any mode, order 3-5) or TTMc (order 3-4) einsum with
+    small, often odd / ragged extents and a random processor count."""
+    order = int(rng.integers(3, 6))
+    modes = "ijklm"[:order]
+    ext = {c: int(rng.integers(2, 13 if order > 3 else 40)) for c in modes}
+    if rng.random() < 0.6:
+        m = int(rng.integers(0, order))
+        R = int(rng.integers(1, 40))
+        ext["a"] = R
+        ins = [modes] + [c + "a" for c in modes if c != modes[m]]
+        e = ",".join(ins) + "->" + modes[m] + "a"
+    else:
+        order = min(order, 4)
+        modes = modes[:order]
+        ext = {c: ext[c] for c in modes}
+        ranks = "bcd"[:order - 1]
+        for r in ranks:
+            ext[r] = int(rng.integers(1, 12))
+        ins = [modes] + [c + r for c, r in zip(modes[1:], ranks)]
+        e = ",".join(ins) + "->" + modes[0] + ranks
+    P = int(rng.choice([1, 2, 3, 4, 6, 8]))
+    return e, ext, P
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_einsums_match_oracle(eb, seed):
+    """Randomised parity: random MTTKRP / TTMc einsums, extents and P through
+    the executor (fused kernels, TTM steps, generic fallbacks, reductions and
+    redistributions on virtual ranks) against the oracle's naive loop."""
+    rng = np.random.default_rng(1000 + seed)
+    e, ext, P = _random_case(rng)
+    ops = oracle.seeded_inputs(e, ext, seed)
+    want = oracle.naive_evaluate(e, ext, ops)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    ex.run()
+    check(ex.gather(), want)
+
+
 @pytest.mark.parametrize("name,einsum,ext", DESK, ids=[d[0] for d in DESK])
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
 def test_comm_volumes_match_reference_accounting(eb, name, einsum, ext, P):
