@@ -307,6 +307,220 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   }
 }
 
+// Warp-specialised variant: the two steps run on different warps and hand
+// t0 over through a shared-memory ring guarded by mbarriers — no CTA-wide
+// barrier per stage.  Warps 0..7 (two per SM sub-partition) do step 0 exactly
+// as above and publish their partial t0 tiles; warps 8..11 (one per
+// sub-partition) each own 4 output rows and run step 1 on every published
+// stage; warp 12 issues the TMA boxes.  Per sub-partition per stage: 64 + 16
+// DMMAs, as before, but a slow warp no longer stalls the others.
+constexpr int kWsS0 = 8, kWsS1 = 4, kWsWarps = kWsS0 + kWsS1 + 1;
+constexpr int kWsStages = 6, kWsT0Slots = 2;
+constexpr int kWsT0Bytes = 2 * kK * kPlane;  // [j half][k][16 r][16 b]
+constexpr int kWsSmem = kWsStages * kXBytes + kWsT0Slots * kWsT0Bytes + 1024;
+
+__global__ void __launch_bounds__(kWsWarps * 32, 1)
+    ttm2_ws_kernel(const __grid_constant__ CUtensorMap xmap, const Ttm2Params prm) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_x[kWsStages];
+  __shared__ __align__(8) uint64_t empty_x[kWsStages];
+  __shared__ __align__(8) uint64_t full_t[kWsT0Slots];
+  __shared__ __align__(8) uint64_t empty_t[kWsT0Slots];
+
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+  uint8_t* const t0s = sbase + kWsStages * kXBytes;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, l = lane & 3;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(smem_addr(&full_x[s]), 1);
+      mbar_init(smem_addr(&empty_x[s]), kWsS0);
+    }
+    for (int s = 0; s < kWsT0Slots; ++s) {
+      mbar_init(smem_addr(&full_t[s]), kWsS0);
+      mbar_init(smem_addr(&empty_t[s]), kWsS1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kWsS0 + kWsS1) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch_desc(&xmap);
+      uint32_t it = 0;
+      for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+        const int p = (int)(item / prm.mtiles);
+        const int r0 = (int)(item % prm.mtiles) * kRows;
+        for (int64_t kc = 0; kc < prm.KC; ++kc, ++it) {
+          const int st = it % kWsStages;
+          if (it >= (uint32_t)kWsStages)
+            mbar_wait(smem_addr(&empty_x[st]), ((it / kWsStages) - 1) & 1);
+          const uint32_t fb = smem_addr(&full_x[st]);
+          mbar_expect_tx(fb, kXBytes);
+          tma_load_4d(base + st * kXBytes, &xmap, fb, r0, 0, (int)(kc * kK), p);
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp < kWsS0) {
+    // ------------------------------------------------------------- step 0
+    const int kk = warp >> 1, jh = warp & 1;
+    double u1[2][4][2];
+#pragma unroll
+    for (int b16 = 0; b16 < 2; ++b16)
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) {
+          const int64_t j = 32 * jh + 16 * b16 + 2 * l + (s & 1) + 8 * (s >> 1);
+          const int64_t n = 8 * nj + g;
+          u1[b16][s][nj] = (j < prm.Q1 && n < prm.N1) ? __ldg(prm.U1 + j * prm.ldu1 + n) : 0.0;
+        }
+    uint32_t offa[4][2];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int j = 32 * jh + 2 * l + (s & 1) + 8 * (s >> 1);
+        const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (j & 7));
+        offa[s][mi] = (uint32_t)(kk * kJ + j) * 128u + chunk * 16u + (g & 1) * 8u;
+      }
+    uint32_t offw[2][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int r = 8 * mi + g;
+        const uint32_t chunk = (uint32_t)((4 * nj + l) ^ (4 * (r & 1)) ^ (2 * kk));
+        offw[mi][nj] = (uint32_t)(jh * kK + kk) * kPlane + (uint32_t)r * 128u + chunk * 16u;
+      }
+    uint32_t it = 0;
+    for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+      for (int64_t kc = 0; kc < prm.KC; ++kc, ++it) {
+        const int st = it % kWsStages;
+        mbar_wait(smem_addr(&full_x[st]), (it / kWsStages) & 1);
+        const uint8_t* xs = sbase + st * kXBytes;
+        double t[2][2][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) t[mi][nj][0] = t[mi][nj][1] = 0.0;
+#pragma unroll
+        for (int b16 = 0; b16 < 2; ++b16)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            double a[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+              a[mi] = *reinterpret_cast<const double*>(xs + offa[s][mi] + b16 * 16 * 128);
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int nj = 0; nj < 2; ++nj)
+                dmma884(t[mi][nj][0], t[mi][nj][1], a[mi], u1[b16][s][nj]);
+          }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&empty_x[st]));
+        const int ts = it % kWsT0Slots;
+        if (it >= (uint32_t)kWsT0Slots)
+          mbar_wait(smem_addr(&empty_t[ts]), ((it / kWsT0Slots) - 1) & 1);
+        uint8_t* tb = t0s + ts * kWsT0Bytes;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+            *reinterpret_cast<double2*>(tb + offw[mi][nj]) = make_double2(t[mi][nj][0], t[mi][nj][1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&full_t[ts]));  // release: the partial is in place
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- step 1
+  const int w1 = warp - kWsS0;  // rows 4*w1 .. 4*w1+3 of the tile
+  constexpr int RW = kRows / kWsS1;
+  uint32_t offr[RW][2];
+#pragma unroll
+  for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = RW * w1 + ri;
+      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (4 * (r & 1)) ^ (2 * l));
+      offr[ri][mi] = (uint32_t)l * kPlane + (uint32_t)r * 128u + chunk * 16u + (g & 1) * 8u;
+    }
+  double acc[RW][2][2][2];
+#pragma unroll
+  for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+  uint32_t it = 0;
+  for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+    const int64_t p = item / prm.mtiles;
+    const int64_t r0 = (item % prm.mtiles) * kRows;
+    for (int64_t kc = 0; kc < prm.KC; ++kc, ++it) {
+      double ub[2];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int64_t k = kc * kK + l, c = 8 * nj + g;
+        ub[nj] = (k < prm.Q2 && c < prm.N2) ? __ldg(prm.U2 + k * prm.ldu2 + c) : 0.0;
+      }
+      const int ts = it % kWsT0Slots;
+      mbar_wait(smem_addr(&full_t[ts]), (it / kWsT0Slots) & 1);
+      const uint8_t* tb = t0s + ts * kWsT0Bytes;
+      double a[RW][2];
+#pragma unroll
+      for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+          a[ri][mi] = *reinterpret_cast<const double*>(tb + offr[ri][mi]) +
+                      *reinterpret_cast<const double*>(tb + offr[ri][mi] + kK * kPlane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty_t[ts]));
+#pragma unroll
+      for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+            dmma884(acc[ri][mi][nj][0], acc[ri][mi][nj][1], a[ri][mi], ub[nj]);
+    }
+#pragma unroll
+    for (int ri = 0; ri < RW; ++ri) {
+      const int64_t r = r0 + RW * w1 + ri;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int64_t b = 8 * mi + g;
+        if (r < prm.M && b < prm.N1) {
+          double* dst = prm.out + ((p * prm.M + r) * prm.N1 + b) * prm.N2;
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) {
+            const int64_t c = 8 * nj + 2 * l;
+            if (c + 1 < prm.N2 && (reinterpret_cast<uintptr_t>(dst + c) & 15) == 0) {
+              *reinterpret_cast<double2*>(dst + c) =
+                  make_double2(acc[ri][mi][nj][0], acc[ri][mi][nj][1]);
+            } else {
+              if (c < prm.N2) dst[c] = acc[ri][mi][nj][0];
+              if (c + 1 < prm.N2) dst[c + 1] = acc[ri][mi][nj][1];
+            }
+          }
+        }
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+      }
+    }
+  }
+}
+
 void validate(const eb_ttm2_desc* d) {
   if (!d) throw InvalidError("eb_ttm2: null descriptor");
   if (d->P < 1 || d->Q1 < 1 || d->Q2 < 1 || d->M < 1 || d->N1 < 1 || d->N2 < 1)
@@ -328,6 +542,20 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
   }
   main_kernel_begin(st);
   ttm2_kernel<NW, PIPE><<<prm.G, (NW + 1) * 32, Cfg<NW>::Smem, st>>>(xmap, prm);
+  EB_CUDA(cudaGetLastError());
+  main_kernel_end(st);
+  count_launch();
+}
+
+void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    EB_CUDA(cudaFuncSetAttribute(ttm2_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kWsSmem));
+    attr = true;
+  }
+  main_kernel_begin(st);
+  ttm2_ws_kernel<<<prm.G, kWsWarps * 32, kWsSmem, st>>>(xmap, prm);
   EB_CUDA(cudaGetLastError());
   main_kernel_end(st);
   count_launch();
@@ -367,8 +595,10 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
   const bool pipe = pp && pp[0] == '1';
   if (v && std::atoi(v) == 16)
     pipe ? launch<16, true>(xmap, prm, st) : launch<16, false>(xmap, prm, st);
-  else
+  else if (v && std::atoi(v) == 8)
     pipe ? launch<8, true>(xmap, prm, st) : launch<8, false>(xmap, prm, st);
+  else
+    launch_ws(xmap, prm, st);
 }
 
 }  // namespace
