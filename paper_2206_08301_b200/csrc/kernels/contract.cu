@@ -497,16 +497,20 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
 
   // Per-lane byte offsets inside a 128-B swizzled row for the 4 k-steps of
   // a 16-deep group (see the header comment for the bank argument).
-  //   ROW: lane reads k = 2s + (l&1) + 8(l>>1) of row (..8i+g)
+  //   ROW: lane reads k = 4l + s of row (..8i+g): its four k values are one
+  //        32-B run, fetched as two 16-B loads (chunks 2l, 2l+1 of the row,
+  //        swizzled by g) that each serve two k-steps — half the shared-memory
+  //        load instructions of the DMMA loop; a quarter-warp (rows g, g^1 x
+  //        chunks {0,2,4,6} or {1,3,5,7}) hits 8 distinct 16-B bank groups
   //   COL: lane reads row k = 2l + (s&1) + 8(s>>1), column (..8i+g)
   uint32_t off[4][2];  // [s][odd m8/n8 tile within a 16-wide box]
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (!COL) {
-        const uint32_t chunk = (uint32_t)((s + 4 * (l >> 1)) ^ g);
-        off[s][h] = g * 128 + chunk * 16 + (l & 1) * 8;
+      if (!COL) {  // k = 4l + s (chunk 2l + s/2, half s&1)
+        const uint32_t chunk = (uint32_t)((2 * l + (s >> 1)) ^ g);
+        off[s][h] = g * 128 + chunk * 16 + (s & 1) * 8;
       } else {
         const int kr = 2 * l + (s & 1) + 8 * (s >> 1);
         const uint32_t chunk = (uint32_t)((4 * h + (g >> 1)) ^ (kr & 7));
@@ -564,6 +568,34 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
       mbar_wait(smem_addr(&full_bar[st]), (it / S) & 1);
       const uint8_t* xs = sbase + st * T::kStageBytes;
       const uint8_t* us = xs + T::kXBytes;
+#pragma unroll
+      if constexpr (!COL && !TWO) {  // (TWO sits at the register cap: 8-B loads)
+#pragma unroll
+        for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
+#pragma unroll
+          for (int sp = 0; sp < 2; ++sp) {  // k-steps 2sp, 2sp+1
+            const uint32_t rowoff = (uint32_t)g * 128u + ((uint32_t)((2 * l + sp) ^ g) << 4);
+            double2 a2[MI], b2[NT];
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+              const int m8 = wm * MI + i;
+              a2[i] = *reinterpret_cast<const double2*>(xs + (b16 * OS + os) * MT * 128 +
+                                                        m8 * 8 * 128 + rowoff);
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+              b2[j] = *reinterpret_cast<const double2*>(us + b16 * NT * 8 * 128 + j * 8 * 128 +
+                                                        rowoff);
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a2[i].x, b2[j].x);
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a2[i].y, b2[j].y);
+          }
+      } else
 #pragma unroll
       for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
 #pragma unroll
