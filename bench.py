@@ -391,6 +391,8 @@ def main():
         elif mi > 0:
             ins = build(pinned=(world == 1))
         ex.stage(_stage_list(ins, shared, dimtree and mi == 1))
+        # reductions on a side stream: mode m's allreduce overlaps mode m+1
+        ex.set_async_reduce(True)
         execs.append(ex)
         inputs.append(ins)
         x_shared.append(shared)
@@ -404,9 +406,11 @@ def main():
             if not execs[0].run_pair(execs[1]):
                 raise RuntimeError("dimension-tree pair did not qualify")
             execs[2].run()
-            return
-        for ex in execs:
-            ex.run()
+        else:
+            for ex in execs:
+                ex.run()
+        for ex in execs:  # the step ends when every reduction has landed
+            ex.join()
 
     for _ in range(args.warmup):
         step()
@@ -559,10 +563,14 @@ def _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree):
     m1.share_input(2, ex0, 2)
     m1.stage([None, inputs[1][1], None])
 
+    m1.set_async_reduce(True)
+
     def step():
         if not ex0.run_pair(m1):
             raise RuntimeError("dimension-tree pair did not qualify")
         ex2.run()
+        for ex in (ex0, m1, ex2):
+            ex.join()
 
     for _ in range(args.warmup):
         step()

@@ -173,6 +173,14 @@ int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
 int eb_exec_share_input(eb_exec* dst, int k_dst, eb_exec* src, int k_src);
 /* all terms: local contractions + reductions + redistributions, device only */
 int eb_exec_run(eb_exec* h);
+/* Reductions on a side stream: with on = 1 a run's allreduces are issued on
+ * an executor-owned stream (after the local contractions), so they overlap
+ * work the caller queues next on `stream` (e.g. the next mode of a sweep);
+ * eb_exec_join(h) then makes `stream` wait for them.  Later terms of the same
+ * schedule, eb_exec_gather and the next eb_exec_run join implicitly.  Off by
+ * default: every operation is then ordered on `stream`. */
+int eb_exec_set_async_reduce(eb_exec* h, int on);
+int eb_exec_join(eb_exec* h);
 /* CP sweep dimension tree: run `mode0` (ijk,ja,ka->ia) and `mode1`
  * (ijk,ia,ka->ja, X and the k factor shared from mode0 with
  * eb_exec_share_input, same grid, same stream) in one pass over X with

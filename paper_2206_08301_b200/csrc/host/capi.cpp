@@ -461,6 +461,20 @@ int eb_exec_run(eb_exec* h) {
   return exec_guard([&] { h->exec->execute(); });
 }
 
+int eb_exec_set_async_reduce(eb_exec* h, int on) {
+  return exec_guard([&] {
+    if (!h) throw eb::InvalidError("eb_exec_set_async_reduce: null handle");
+    h->exec->set_async_reduce(on != 0);
+  });
+}
+
+int eb_exec_join(eb_exec* h) {
+  return exec_guard([&] {
+    if (!h) throw eb::InvalidError("eb_exec_join: null handle");
+    h->exec->join();
+  });
+}
+
 int eb_exec_run_pair(eb_exec* mode0, eb_exec* mode1, int* fused) {
   return exec_guard([&] {
     if (!mode0 || !mode1) throw eb::InvalidError("eb_exec_run_pair: null handle");

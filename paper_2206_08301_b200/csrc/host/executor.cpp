@@ -334,7 +334,14 @@ ScheduleExecutor::ScheduleExecutor(Pipeline pipe, Transport* transport, cudaStre
 }
 
 ScheduleExecutor::~ScheduleExecutor() {
+  if (comm_pending_) cudaStreamWaitEvent(stream_, ev_comm_, 0);  // no throwing in a destructor
   cudaStreamSynchronize(stream_);
+  if (comm_stream_) {
+    cudaStreamSynchronize(comm_stream_);
+    cudaStreamDestroy(comm_stream_);
+  }
+  if (ev_compute_) cudaEventDestroy(ev_compute_);
+  if (ev_comm_) cudaEventDestroy(ev_comm_);
   run_arena_.release(stream_);
   input_arena_.release(stream_);
   cudaFreeAsync(workspace_, stream_);
@@ -687,8 +694,34 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
   return out;
 }
 
+void ScheduleExecutor::join() {
+  if (!comm_pending_) return;
+  cuda_ok(cudaStreamWaitEvent(stream_, ev_comm_, 0), "join: wait for the reduction");
+  comm_pending_ = false;
+}
+
+std::int64_t ScheduleExecutor::reduce(const TensorPlacement& place, const ReductionGroup& grp,
+                                      std::vector<DevBlock>& blocks, bool last_term) {
+  if (!async_reduce_ || grp.depth <= 1)
+    return transport_->allreduce(place, grp, blocks, comm_.per_rank_sent, stream_);
+  if (!comm_stream_) {
+    cuda_ok(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+    cuda_ok(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "event");
+  }
+  join();  // one reduction in flight per executor
+  cuda_ok(cudaEventRecord(ev_compute_, stream_), "event record");
+  cuda_ok(cudaStreamWaitEvent(comm_stream_, ev_compute_, 0), "stream wait");
+  const std::int64_t v = transport_->allreduce(place, grp, blocks, comm_.per_rank_sent, comm_stream_);
+  cuda_ok(cudaEventRecord(ev_comm_, comm_stream_), "event record");
+  comm_pending_ = true;
+  if (!last_term) join();  // the next term reads it on the compute stream
+  return v;
+}
+
 void ScheduleExecutor::execute() {
   if (!staged_) fail(errc::invalid_argument, "execute: inputs not staged");
+  join();  // the previous run's reduction still owns its output blocks
   run_arena_.release(stream_);
   store_.clear();
   comm_ = CommStats{};
@@ -782,8 +815,8 @@ void ScheduleExecutor::execute() {
         }
       }
     }
-    const std::int64_t v =
-        transport_->allreduce(out_place, term.reduction, out_blocks, comm_.per_rank_sent, stream_);
+    const std::int64_t v = reduce(out_place, term.reduction, out_blocks,
+                                  &term == &pipe_.schedule.terms.back());
     if (term.reduction.depth > 1) {
       comm_.events.push_back({"allreduce", term.index, term.statement.output, v});
       comm_.allreduce_volume += v;
@@ -850,6 +883,7 @@ bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
   }
 
   for (ScheduleExecutor* e : {this, &m1}) {
+    e->join();
     e->run_arena_.release(e->stream_);
     e->store_.clear();
     e->comm_ = CommStats{};
@@ -877,8 +911,7 @@ bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
   };
   for (const Side& sd : {Side{this, &t0, &out0}, Side{&m1, &t1, &out1}}) {
     const TensorPlacement& place = sd.t->placement_of(sd.t->statement.output);
-    const std::int64_t v = sd.e->transport_->allreduce(place, sd.t->reduction, *sd.out,
-                                                       sd.e->comm_.per_rank_sent, sd.e->stream_);
+    const std::int64_t v = sd.e->reduce(place, sd.t->reduction, *sd.out, true);
     if (sd.t->reduction.depth > 1) {
       sd.e->comm_.events.push_back({"allreduce", sd.t->index, sd.t->statement.output, v});
       sd.e->comm_.allreduce_volume += v;
@@ -893,6 +926,7 @@ std::vector<std::int64_t> ScheduleExecutor::output_shape() const {
 }
 
 void ScheduleExecutor::gather(double* host_out) {
+  join();
   const TermPlan& last = pipe_.schedule.terms.back();
   const TensorPlacement& place = last.placement_of(last.statement.output);
   auto& blocks = store_.at({last.index, last.statement.output});

@@ -114,6 +114,12 @@ class ScheduleExecutor {
   // reduction group.  Returns false (nothing run) when the pair does not
   // qualify; the caller then runs both executors separately.
   bool execute_pair(ScheduleExecutor& mode1);
+  // Reductions on a side stream (opt-in): a term's allreduce then overlaps
+  // whatever the caller queues next on the compute stream (e.g. the next
+  // mode of a sweep); join() orders the compute stream after it.  Later terms
+  // of the same schedule, gather() and the next execute() join implicitly.
+  void set_async_reduce(bool on) { async_reduce_ = on; }
+  void join();
   // Canonical output blocks to host (virtual, or rank 0 over NCCL).
   void gather(double* host_out);
   void verify(const std::vector<const double*>& global_inputs, const double* host_out,
@@ -142,6 +148,8 @@ class ScheduleExecutor {
                       const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
   DevBlock run_step(const TermPlan& term, int sid, std::int64_t rank,
                     const std::map<std::string, const DevBlock*>& at_hand);
+  std::int64_t reduce(const TensorPlacement& place, const ReductionGroup& grp,
+                      std::vector<DevBlock>& blocks, bool last_term);
 
   Pipeline pipe_;
   Transport* transport_;
@@ -156,6 +164,9 @@ class ScheduleExecutor {
   std::size_t workspace_bytes_ = 0;
   CommStats comm_;
   int launches_fused_ = 0, launches_ttm_ = 0, launches_generic_ = 0;
+  bool async_reduce_ = false, comm_pending_ = false;
+  cudaStream_t comm_stream_ = nullptr;
+  cudaEvent_t ev_compute_ = nullptr, ev_comm_ = nullptr;
   // EB_FUSE_TTM2=0 runs TTM-pair terms as two eb_contract launches (A/B checks)
   bool fuse_ttm_ = [] {
     const char* v = std::getenv("EB_FUSE_TTM2");

@@ -250,6 +250,30 @@ def test_exec_run_pair_cp_sweep(eb, P):
     check(ex1.gather(), got1)
 
 
+@pytest.mark.parametrize("name,einsum,ext",
+                         [d for d in DESK if d[0] in ("2MM", "3MM", "MTTKRP-O3-M1", "MTTKRP-O5-M0")],
+                         ids=["2MM", "3MM", "MTTKRP-O3-M1", "MTTKRP-O5-M0"])
+@pytest.mark.parametrize("P", [4, 8])
+def test_async_reduce_matches_ordered(eb, name, einsum, ext, P):
+    """Reductions on the side stream (eb_exec_set_async_reduce): a sweep of
+    runs with joins must give the ordered run's output bit for bit, including
+    multi-term schedules whose later terms consume a reduced output."""
+    ops = oracle.seeded_inputs(einsum, ext, 9)
+    ex = eb.Executor(einsum, ext, P)
+    ex.stage(ops)
+    ex.run()
+    want = ex.gather()
+    ex2 = eb.Executor(einsum, ext, P)
+    ex2.stage(ops)
+    ex2.set_async_reduce(True)
+    for _ in range(3):
+        ex2.run()
+    ex2.join()
+    got = ex2.gather()
+    assert np.array_equal(got, want)
+    assert ex2.stats()["allreduce_volume"] == ex.stats()["allreduce_volume"]
+
+
 def test_exec_run_pair_falls_back_when_not_shared(eb):
     ext = dict(i=128, j=32, k=32, a=8)
     X = oracle.random_tensor((128, 32, 32), 0)
