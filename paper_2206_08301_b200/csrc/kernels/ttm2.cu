@@ -383,22 +383,23 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
           const int64_t n = 8 * nj + g;
           u1[b16][s][nj] = (j < prm.Q1 && n < prm.N1) ? __ldg(prm.U1 + j * prm.ldu1 + n) : 0.0;
         }
-    uint32_t offa[4][2];
+    // A fragments of the two row tiles come from one 16-B load: row tile mi
+    // holds rows 2g + mi (rows interleaved, not 8-row blocks), so lane (g, l)
+    // reads rows 2g, 2g+1 of X row j as chunk g of that 128-B row (swizzled
+    // by j & 7 = 2l + (s&1): a quarter-warp covers 8 distinct 16-B groups)
+    uint32_t offa[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const int j = 32 * jh + 2 * l + (s & 1) + 8 * (s >> 1);
-        const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (j & 7));
-        offa[s][mi] = (uint32_t)(kk * kJ + j) * 128u + chunk * 16u + (g & 1) * 8u;
-      }
+    for (int s = 0; s < 4; ++s) {
+      const int j = 32 * jh + 2 * l + (s & 1) + 8 * (s >> 1);
+      offa[s] = (uint32_t)(kk * kJ + j) * 128u + (uint32_t)(g ^ (j & 7)) * 16u;
+    }
     uint32_t offw[2][2];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) {
-        const int r = 8 * mi + g;
-        const uint32_t chunk = (uint32_t)((4 * nj + l) ^ (4 * (r & 1)) ^ (2 * kk));
+        const int r = 2 * g + mi;
+        const uint32_t chunk = (uint32_t)((4 * nj + l) ^ (4 * ((r >> 1) & 1)) ^ (2 * kk));
         offw[mi][nj] = (uint32_t)(jh * kK + kk) * kPlane + (uint32_t)r * 128u + chunk * 16u;
       }
     uint32_t it = 0;
@@ -416,15 +417,12 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
         for (int b16 = 0; b16 < 2; ++b16)
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
-            double a[2];
+            const double2 a2 = *reinterpret_cast<const double2*>(xs + offa[s] + b16 * 16 * 128);
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-              a[mi] = *reinterpret_cast<const double*>(xs + offa[s][mi] + b16 * 16 * 128);
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-              for (int nj = 0; nj < 2; ++nj)
-                dmma884(t[mi][nj][0], t[mi][nj][1], a[mi], u1[b16][s][nj]);
+            for (int nj = 0; nj < 2; ++nj) {
+              dmma884(t[0][nj][0], t[0][nj][1], a2.x, u1[b16][s][nj]);
+              dmma884(t[1][nj][0], t[1][nj][1], a2.y, u1[b16][s][nj]);
+            }
           }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_addr(&empty_x[st]));
@@ -453,7 +451,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
       const int r = RW * w1 + ri;
-      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (4 * (r & 1)) ^ (2 * l));
+      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (4 * ((r >> 1) & 1)) ^ (2 * l));
       offr[ri][mi] = (uint32_t)l * kPlane + (uint32_t)r * 128u + chunk * 16u + (g & 1) * 8u;
     }
   double acc[RW][2][2][2];
