@@ -342,6 +342,32 @@ def _random_case(rng):
     return e, ext, P
 
 
+@pytest.mark.parametrize("fmt", ["npy", "jsonl"])
+def test_run_json_tensor_files(eb, tmp_path, fmt):
+    """einplan_run_json with input_paths / dump_output (tensor.cpp:76-103):
+    the reference's jsonl format and the binary .npy side format (for GB-scale
+    operands) give the oracle's result for the given inputs."""
+    e, ext = "ijk,ja,ka->ia", dict(i=40, j=33, k=18, a=12)
+    rng = np.random.default_rng(5)
+    ops = [rng.uniform(-1, 1, oracle.shape_of(t, ext)) for t in e.split("->")[0].split(",")]
+    paths = []
+    for k, a in enumerate(ops):
+        pth = str(tmp_path / f"in{k}.{fmt}")
+        if fmt == "npy":
+            np.save(pth, a)
+        else:
+            with open(pth, "w") as f:
+                f.write(json.dumps({"shape": list(a.shape)}) + "\n")
+                f.writelines(repr(float(v)) + "\n" for v in a.ravel())
+        paths.append(pth)
+    out = str(tmp_path / f"out.{fmt}")
+    st, rep = eb.Session(e, ext).run_json(4, 1024.0, seed=0, verify=True,
+                                          input_paths=",".join(paths), dump_output=out)
+    assert st == 0 and json.loads(rep)["verification"]["pass"]
+    got = np.load(out) if fmt == "npy" else np.loadtxt(out, skiprows=1)
+    check(np.asarray(got).reshape(40, 12), oracle.naive_evaluate(e, ext, ops))
+
+
 @pytest.mark.parametrize("seed", range(24))
 def test_random_einsums_match_oracle(eb, seed):
     """Randomised parity: random MTTKRP / TTMc einsums, extents and P through
