@@ -178,11 +178,30 @@ __device__ __forceinline__ void fold_krp(double (&t)[MI][NT][2], double (&m)[MI]
 
 // Store one row tile's register accumulators into partial slot (sg, ks) of
 // this CTA and clear them.
-template <int MI, int NT, int MT, int WM, int SPL>
+// VC (vectorised COL fragments): accumulator tile i holds rows
+// 16(i/2) + 2g + (i%2), tile j columns 16(j/2) + 2c' + (j%2) — lane (g, l)'s
+// element e of tiles (2q, 2q+1) are columns 16q + 4l + 2e + {0, 1}.
+__device__ __forceinline__ int vc_row(int i, int g) { return 16 * (i >> 1) + 2 * g + (i & 1); }
+
+template <int MI, int NT, int MT, int WM, int SPL, bool VC = false>
 __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const ContractParams& prm,
                                               int sg, int wm, int split, int g, int l) {
   double* dst = prm.out +
                 (((int64_t)blockIdx.x * prm.segmax + sg) * SPL + split) * (int64_t)MT * (NT * 8);
+  if constexpr (VC) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int q = 0; q < NT / 2; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = wm * WM + vc_row(i, g);
+          *reinterpret_cast<double2*>(dst + row * (NT * 8) + 16 * q + 4 * l + 2 * e) =
+              make_double2(acc[i][2 * q][e], acc[i][2 * q + 1][e]);
+          acc[i][2 * q][e] = acc[i][2 * q + 1][e] = 0.0;
+        }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -260,6 +279,9 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   constexpr int SPL = KS * OS;  // partial slots per row tile
   using T = Tile<COL, MT, NT, KD, OS>;
   constexpr int S = T::kStages;
+  // COL with paired row and column tiles: both fragments of a tile pair come
+  // from one 16-B load (see vc_row)
+  constexpr bool VC = COL && MI % 2 == 0 && NT % 2 == 0;
   static_assert(!BATCHED || KS == 1, "BATCHED writes each unit once");
 
   extern __shared__ uint8_t smem_raw[];
@@ -546,7 +568,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
         fold_krp<MI, NT>(acc, macc, krow);
       }
       if (mt != cur_mt) {
-        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
+        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL, VC>(macc, prm, seg, wm, ks + KS * os, g, l);
         ++seg;
         cur_mt = mt;
       }
@@ -559,8 +581,13 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
                                                          T::kXBytes + T::kUBytes);
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        krow[j][0] = sc[os * NT * 8 + j * 8 + 2 * l];
-        krow[j][1] = sc[os * NT * 8 + j * 8 + 2 * l + 1];
+        if constexpr (VC) {
+          krow[j][0] = sc[os * NT * 8 + 16 * (j >> 1) + 4 * l + (j & 1)];
+          krow[j][1] = sc[os * NT * 8 + 16 * (j >> 1) + 4 * l + 2 + (j & 1)];
+        } else {
+          krow[j][0] = sc[os * NT * 8 + j * 8 + 2 * l];
+          krow[j][1] = sc[os * NT * 8 + j * 8 + 2 * l + 1];
+        }
       }
     }
     for (int64_t kc = kc_begin; kc < kc_end; ++kc, ++it) {
@@ -595,6 +622,35 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
 #pragma unroll
               for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], a2[i].y, b2[j].y);
           }
+      } else if constexpr (VC) {
+        // lane (g, l) reads row k = 2l + (s&1) + 8(s>>1) of a 16-wide box,
+        // chunk g (two consecutive m / n): a quarter-warp's rows have swizzle
+        // phases 2l + (s&1), so its 8 chunks g ^ phase are distinct
+#pragma unroll
+        for (int b16 = ks; b16 < KD / 16; b16 += KS)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const int kr = 2 * l + (s & 1) + 8 * (s >> 1);
+            const uint32_t rowoff = (uint32_t)(b16 * 16 + kr) * 128u + ((uint32_t)(g ^ (kr & 7)) << 4);
+            double2 a2[MI / 2], b2[NT / 2];
+#pragma unroll
+            for (int pi = 0; pi < MI / 2; ++pi)
+              a2[pi] = *reinterpret_cast<const double2*>(
+                  xs + ((wm * MI / 2 + pi) * OS + os) * KD * 128 + rowoff);
+#pragma unroll
+            for (int q = 0; q < NT / 2; ++q)
+              b2[q] = *reinterpret_cast<const double2*>(us + q * KD * 128 + rowoff);
+#pragma unroll
+            for (int pi = 0; pi < MI / 2; ++pi)
+#pragma unroll
+              for (int q = 0; q < NT / 2; ++q) {
+                dmma884(acc[2 * pi][2 * q][0], acc[2 * pi][2 * q][1], a2[pi].x, b2[q].x);
+                dmma884(acc[2 * pi][2 * q + 1][0], acc[2 * pi][2 * q + 1][1], a2[pi].x, b2[q].y);
+                dmma884(acc[2 * pi + 1][2 * q][0], acc[2 * pi + 1][2 * q][1], a2[pi].y, b2[q].x);
+                dmma884(acc[2 * pi + 1][2 * q + 1][0], acc[2 * pi + 1][2 * q + 1][1], a2[pi].y,
+                        b2[q].y);
+              }
+          }
       } else
 #pragma unroll
       for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
@@ -628,7 +684,32 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
     }
-    if (BATCHED) {
+    if constexpr (BATCHED && VC) {
+      // out[p][m][col0 + n] from the interleaved tiles (see vc_row)
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int64_t row = mt * MT + wm * WM + vc_row(i, g);
+        if (row < prm.M) {
+          double* dst = prm.out + (o * prm.M + row) * prm.ldo + prm.col0;
+#pragma unroll
+          for (int q = 0; q < NT / 2; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = 16 * q + 4 * l + 2 * e;
+              const int gc = prm.col0 + c;
+              if (gc + 1 < prm.R && ((reinterpret_cast<uintptr_t>(dst + c) & 15) == 0)) {
+                *reinterpret_cast<double2*>(dst + c) =
+                    make_double2(acc[i][2 * q][e], acc[i][2 * q + 1][e]);
+              } else {
+                if (gc < prm.R) dst[c] = acc[i][2 * q][e];
+                if (gc + 1 < prm.R) dst[c + 1] = acc[i][2 * q + 1][e];
+              }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      }
+    } else if (BATCHED) {
       // out[p][m][col0 + n], guarded at the ragged row / column edges.
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
@@ -659,7 +740,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
       if constexpr (TWO)
         emit_two<MI, NT, NWM, MT, WM>(acc, red2, prm, cur_mt, cur_o, o_kc0, n_emit++, wm, g, l, lane);
       fold_krp<MI, NT>(acc, macc, krow);
-      flush_partial<MI, NT, MT, WM, SPL>(macc, prm, seg, wm, ks + KS * os, g, l);
+      flush_partial<MI, NT, MT, WM, SPL, VC>(macc, prm, seg, wm, ks + KS * os, g, l);
     }
   }
 }
