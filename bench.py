@@ -200,23 +200,34 @@ class ClockSampler:
 
 # ------------------------------------------------------- reference arm --
 
-def _ref_sample_step(threads: int, rows: int):
-    """One bounded sample of the C2 sweep on the reference implementation:
+# i-rows of X per reference run() in the CPU samples (a few seconds of
+# single-threaded reference work each); every config's output mode 0 (and
+# C2's sweep) is a sum over independent i-slabs, so a slab is a faithful,
+# proportionally smaller instance of the same computation
+REF_SLAB_ROWS = {"C1": 16, "C2": 8, "C3": 1, "C4": 4, "C5": 1}
+
+
+def _ref_sample_step(threads: int, rows: int, config: str = "C2"):
+    """One bounded sample of `config` on the reference implementation:
     `threads` concurrent reference run() calls (P=1), each on its own slab of
-    `rows` i-rows of X for all three modes.  Returns (flops, seconds)."""
+    `rows` i-rows of X (C2: all three modes).  Returns (flops, seconds)."""
     import oracle
-    from tests.configs import CONFIGS, c2_inputs
-    c = CONFIGS["C2"]
+    from tests.configs import CONFIGS
+    c = CONFIGS[config]
     work = []
     flops_per_mode = {}
     ext = dict(c["extents"](1))
     ext["i"] = rows
     for t in range(threads):
-        X = oracle.random_tensor((rows, 1024, 1024), 100 + t)
+        xin = c["einsums"][0].split("->")[0].split(",")[0]
+        X = oracle.random_tensor(oracle.shape_of(xin, ext), 100 + t)
         per_mode = []
         for mode, e in enumerate(c["einsums"]):
             ins, _ = oracle.parse(e)
-            ops = [X] + [oracle.random_tensor(oracle.shape_of(s, ext), {"i": 1, "j": 2, "k": 3}[s[0]])
+            seeds = ({"i": 1, "j": 2, "k": 3} if config == "C2"
+                     else {s: k + 1 for k, s in enumerate(ins[1:])})
+            ops = [X] + [oracle.random_tensor(oracle.shape_of(s, ext),
+                                              seeds[s[0]] if config == "C2" else seeds[s])
                          for s in ins[1:]]
             per_mode.append((e, ext, ops))
             if e not in flops_per_mode:
@@ -247,31 +258,28 @@ def run_reference(args, rank, world):
     import oracle
     if not oracle.ref_available():
         oracle.build(ref=True)
-    if args.config != "C2":
-        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for C2"}))
-        return 0
     cores = os.cpu_count() or 1
     threads = max(1, min(cores, 32))
-    rows = 8
+    rows = REF_SLAB_ROWS[args.config]
     for _ in range(args.warmup):
-        _ref_sample_step(threads, rows)
+        _ref_sample_step(threads, rows, args.config)
     tot_f, tot_s = 0, 0.0
     for _ in range(args.steps):
-        f, s = _ref_sample_step(threads, rows)
+        f, s = _ref_sample_step(threads, rows, args.config)
         tot_f += f
         tot_s += s
     value = tot_f / tot_s / 1e9
-    sample = (f"C2 sweep sample per step: {threads} concurrent reference run() calls (P=1, "
+    sample = (f"{args.config} sample per step: {threads} concurrent reference run() calls (P=1, "
               f"single-threaded each, oracle/_ref built from the reference sources), each on an "
-              f"{rows}-row i-slab of X (X[{rows},1024,1024], all 3 modes); GFLOP/s = reference "
-              f"tree flops / wall time")
+              f"{rows}-row i-slab of X{' (all 3 modes)' if args.config == 'C2' else ''}; "
+              f"GFLOP/s = reference tree flops / wall time")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference random_tensor, mt19937_64 seed 0 / factor seeds 1,2,3)",
-        "config": {"workload": workload_label("C2"), "sample_rows_per_thread": rows,
+        "config": {"workload": workload_label(args.config), "sample_rows_per_thread": rows,
                    "threads": threads},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads,
                          "kind": cpu_kind(), "sample": sample},
@@ -284,11 +292,18 @@ def run_reference(args, rank, world):
 
 def workload_label(name):
     return {
+        "C1": "C1: order-3 MTTKRP mode-0, X 512^3, R=24",
         "C2": "C2: order-3 CP-ALS MTTKRP sweep (modes 0,1,2), X 1024^3 fp64, factors 1024x32",
+        "C3": "C3: order-5 MTTKRP mode-0, X 64^5, R=24",
+        "C4": "C4: order-3 TTMc mode-0, X 1024^3, U1/U2 1024x64 (binary chain)",
+        "C5": "C5: order-5 TTMc mode-0, X (64P)x64^4, factors 64x16 (weak scaling)",
     }.get(name, name)
 
 
-def cpu_baseline_leg():
+CPU_LEG_ROWS = {"C1": 64, "C2": 16, "C3": 1, "C4": 8, "C5": 1}
+
+
+def cpu_baseline_leg(config="C2"):
     """Rank 0, N = 1: the reference (or the oracle port) on a bounded sample,
     single-threaded as the reference is (README.md:149-150)."""
     import oracle
@@ -298,10 +313,12 @@ def cpu_baseline_leg():
         except Exception:
             pass
     if oracle.ref_available():
-        f, s = _ref_sample_step(1, 16)
+        rows = CPU_LEG_ROWS[config]
+        f, s = _ref_sample_step(1, rows, config)
+        what = "sweep (3 modes)" if config == "C2" else "run"
         return {"value": f / s / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
-                "sample": "C2 sweep (3 modes) on X[0:16,:,:] (16 of 1024 i-rows), reference "
-                          "run() at P=1, one host thread (the reference is single-threaded); "
+                "sample": f"{config} {what} on an X slab of {rows} i-rows, reference run() at "
+                          "P=1, one host thread (the reference is single-threaded); "
                           f"{s:.1f} s of CPU work"}
     # Port: the C restatement on a smaller slab.
     ext = dict(i=4, j=1024, k=1024, a=32)
@@ -543,7 +560,7 @@ def main():
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_leg()
+        line["cpu_baseline"] = cpu_baseline_leg(args.config)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
