@@ -64,7 +64,10 @@ def workload(name: str, P: int):
     def seeded_builder(e, shared_seed=None):
         ins, _ = e.split("->")[0].split(","), None
 
-        def build(pinned, skip_x=False):
+        def build(pinned, skip_x=False, ex=None):
+            """Host operands: global tensors, or (ex given: one process per
+            GPU) just the boxes this rank holds — no rank materialises the
+            global X (C5 at P = 8: 69 GB)."""
             out = []
             for k, t in enumerate(ins):
                 if k == 0 and skip_x:
@@ -72,7 +75,12 @@ def workload(name: str, P: int):
                     continue
                 shape = tuple(ext[s] for s in t)
                 seed = k if shared_seed is None else (0 if k == 0 else C2_FACTOR_SEED[t[0]])
-                out.append(_fill(shape, seed, pinned and k == 0))
+                if ex is not None:
+                    base, bshape = ex.block(k)
+                    buf = _host_buffer(int(np.prod(bshape)), pinned and k == 0)
+                    out.append(eb.random_block(seed, shape, base, bshape, out=buf))
+                else:
+                    out.append(_fill(shape, seed, pinned and k == 0))
             return out
         return build
 
@@ -91,6 +99,15 @@ def workload(name: str, P: int):
 
 
 _pinned_keep = []
+
+
+def _host_buffer(n, pinned):
+    if pinned:
+        import torch
+        t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        _pinned_keep.append(t)
+        return t.numpy()
+    return np.empty(n, dtype=np.float64)
 
 
 def _fill(shape, seed, pinned):
@@ -389,8 +406,10 @@ def main():
     stream = torch.cuda.Stream()
     execs, inputs, grids, flops_tree = [], [], [], 0
     x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
+    # one process per GPU: stage only this rank's boxes (EB_BENCH_BLOCKS=1
+    # forces it for a single NCCL rank, to exercise the path on one GPU)
+    blockmode = world > 1 or (use_nccl and os.environ.get("EB_BENCH_BLOCKS") == "1")
     for mi, (e, ext, build) in enumerate(modes):
-        ins = build(pinned=(world == 1)) if mi == 0 else None
         if mi == 0:
             ex = eb.Executor(e, ext, P, 1024.0, rank if use_nccl else -1, nccl_id,
                              stream=stream.cuda_stream)
@@ -399,15 +418,15 @@ def main():
         shared = False
         if mi > 0 and args.config == "C2":
             # the CP-ALS sweep: one X in HBM for the three modes (eb_exec_share_input)
-            ins = build(pinned=False, skip_x=True)
+            ins = build(pinned=False, skip_x=True, ex=ex if blockmode else None)
             ins[0] = inputs[0][0]
             ex.share_input(0, execs[0], 0)
             shared = True
             if dimtree and mi == 1:  # mode 1 also takes mode 0's C blocks (same tensor)
                 ex.share_input(2, execs[0], 2)
-        elif mi > 0:
-            ins = build(pinned=(world == 1))
-        ex.stage(_stage_list(ins, shared, dimtree and mi == 1))
+        else:
+            ins = build(pinned=(world == 1 or blockmode), ex=ex if blockmode else None)
+        _stage(ex, ins, shared, dimtree and mi == 1, blockmode)
         # reductions on a side stream: mode m's allreduce overlaps mode m+1
         ex.set_async_reduce(True)
         execs.append(ex)
@@ -481,8 +500,10 @@ def main():
         h2d = 0
         for ins, ex_, sh in zip(inputs, execs, x_shared):
             # bytes this rank copies: its blocks of every operand it stages
-            h2d += _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh,
-                                 skip2=dimtree and ex_ is execs[1])
+            h2d += (sum(a.nbytes for a in _stage_list(ins, sh, dimtree and ex_ is execs[1])
+                        if a is not None) if blockmode else
+                    _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh,
+                                  skip2=dimtree and ex_ is execs[1]))
         d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
         reps = max(1, min(args.steps, 3))
         if world > 1:
@@ -491,7 +512,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(reps):
             for mi_, (ins, ex_, sh) in enumerate(zip(inputs, execs, x_shared)):
-                ex_.stage(_stage_list(ins, sh, dimtree and mi_ == 1))
+                _stage(ex_, ins, sh, dimtree and mi_ == 1, blockmode)
             step()
             for ex_, out in zip(execs, outs):
                 ex_.gather(out)
@@ -503,7 +524,7 @@ def main():
             dt = float(t.item())
         e2e = {"value": flops_tree / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
-               "host_buffers": "pinned" if world == 1 else "pageable"}
+               "host_buffers": "pinned" if (world == 1 or blockmode) else "pageable"}
         if world == 1:
             # the e2e roofline: the same bytes through one plain pinned H2D copy
             bw = _h2d_gbs(int(h2d))
@@ -578,7 +599,10 @@ def _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree):
     m1 = eb.Executor(ex1.einsum, ex1.extents, stream=stream.cuda_stream, like=ex0)
     m1.share_input(0, ex0, 0)
     m1.share_input(2, ex0, 2)
-    m1.stage([None, inputs[1][1], None])
+    if world > 1:
+        m1.stage_block(1, inputs[1][1])  # same placement as the mode-1 executor
+    else:
+        m1.stage([None, inputs[1][1], None])
 
     m1.set_async_reduce(True)
 
@@ -644,6 +668,16 @@ def _x_bytes(modes, P):
         t = e.split("->")[0].split(",")[0]
         tot += 8 * int(np.prod([ext[c] for c in t])) // P
     return tot
+
+
+def _stage(ex, ins, x_shared, c_shared, blockmode):
+    lst = _stage_list(ins, x_shared, c_shared)
+    if not blockmode:
+        ex.stage(lst)
+        return
+    for k, a in enumerate(lst):
+        if a is not None:
+            ex.stage_block(k, a)
 
 
 def _stage_list(ins, x_shared, c_shared):

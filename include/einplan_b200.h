@@ -139,6 +139,11 @@ int eb_einsum_generic(int n_ops, const char* const* in_indices, const char* out_
  * fills host memory with n values of the mt19937_64(seed) stream starting at
  * element `skip` of that stream. */
 void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip);
+/* the box [base, base + shape) of the row-major tensor random_tensor(gshape,
+ * seed) would produce, written densely to out (one pass over the stream up
+ * to the box's last element; memory O(box)) */
+int eb_random_fill_block(double* out, uint64_t seed, int nd, const int64_t* gshape,
+                         const int64_t* base, const int64_t* shape);
 
 void eb_free(void* p);
 
@@ -167,6 +172,11 @@ void eb_exec_destroy(eb_exec* h);
 /* scatter (executor.cpp:48-65): host global inputs -> this process's blocks */
 int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
 /* a NULL entry in host_inputs keeps that operand's device blocks as they are */
+/* one process = one rank: the box (global base / shape, nd dims) of operand k
+ * this rank holds, and staging from a host buffer holding just that box
+ * (row-major) — no process needs the global tensor */
+int eb_exec_block(eb_exec* h, int k, int64_t* base, int64_t* shape, int* nd);
+int eb_exec_stage_block(eb_exec* h, int k, const double* host_block);
 /* alias operand k_dst of `dst` to the staged device blocks of operand k_src of
  * `src` (same shape and placement on every owned rank, checked); `dst` then
  * stages NULL for it (e.g. one X shared by the three modes of a CP-ALS sweep) */

@@ -89,6 +89,23 @@ class Session:
         return st, _capi.take_string(p)
 
 
+def random_block(seed: int, gshape, base, shape, out: np.ndarray | None = None) -> np.ndarray:
+    """The box [base, base+shape) of random_tensor(gshape, seed), generated
+    without materialising the global tensor (into `out` when given, e.g. a
+    pinned buffer)."""
+    nd = len(gshape)
+    n = int(np.prod(shape))
+    if out is None:
+        out = np.empty(n, dtype=np.float64)
+    out = out.reshape(-1)
+    if out.size != n or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("random_block: out must be a contiguous float64 array of the box size")
+    arr = lambda v: (ctypes.c_int64 * nd)(*[int(x) for x in v])
+    _capi.check(_capi.lib().eb_random_fill_block(out.ctypes.data_as(_capi._dp), seed, nd,
+                                                 arr(gshape), arr(base), arr(shape)))
+    return out.reshape([int(x) for x in shape])
+
+
 def bench_json(scale: float, procs: int, fast_mem: float = 1024.0, seed: int = 1):
     p = ctypes.c_void_p()
     st = _capi.lib().einplan_bench_json(scale, procs, fast_mem, seed, ctypes.byref(p))
@@ -171,6 +188,20 @@ class Executor:
                                           for a in arrs])
         _capi.check(_capi.lib().eb_exec_stage(self._h, ptrs))
         self._keep = arrs  # the copies are asynchronous: keep the sources alive
+
+    def block(self, k: int):
+        """(base, shape) of operand k's box on this process's rank."""
+        base, shape = (ctypes.c_int64 * 16)(), (ctypes.c_int64 * 16)()
+        nd = ctypes.c_int(0)
+        _capi.check(_capi.lib().eb_exec_block(self._h, k, base, shape, ctypes.byref(nd)))
+        return list(base[:nd.value]), list(shape[:nd.value])
+
+    def stage_block(self, k: int, block: np.ndarray):
+        """Stage operand k from a host array holding just this rank's box."""
+        a = np.ascontiguousarray(block, dtype=np.float64)
+        _capi.check(_capi.lib().eb_exec_stage_block(self._h, k, a.ctypes.data_as(_capi._dp)))
+        self._keep_blocks = getattr(self, "_keep_blocks", {})
+        self._keep_blocks[k] = a  # asynchronous copy: keep the source alive
 
     def share_input(self, k: int, src: "Executor", k_src: int):
         """Use ``src``'s staged device blocks for operand ``k`` (no copy)."""

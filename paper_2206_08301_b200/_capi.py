@@ -57,7 +57,8 @@ EXPORTS = [
     "einplan_plan_json", "einplan_run_json", "einplan_bench_json",
     "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_mttkrp2_workspace", "eb_mttkrp2", "eb_ttm2",
     "eb_step_generic",
-    "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host", "eb_free",
+    "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host",
+    "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
     "eb_exec_join", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
@@ -115,6 +116,13 @@ def lib():
         _sig(L, "eb_exec_set_async_reduce", ctypes.c_int, [_vp, ctypes.c_int])
         _sig(L, "eb_exec_join", ctypes.c_int, [_vp])
         _sig(L, "eb_random_fill_host", None, [_dp, _i64, ctypes.c_uint64, _i64])
+        _sig(L, "eb_random_fill_block", ctypes.c_int,
+             [_dp, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+              ctypes.POINTER(_i64)])
+        _sig(L, "eb_exec_block", ctypes.c_int,
+             [_vp, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+              ctypes.POINTER(ctypes.c_int)])
+        _sig(L, "eb_exec_stage_block", ctypes.c_int, [_vp, ctypes.c_int, _dp])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,
              [c, c, _i64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(_vp)])

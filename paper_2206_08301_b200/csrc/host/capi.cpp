@@ -450,6 +450,24 @@ int eb_exec_stage(eb_exec* h, const double* const* host_inputs) {
   });
 }
 
+int eb_exec_block(eb_exec* h, int k, int64_t* base, int64_t* shape, int* nd) {
+  return exec_guard([&] {
+    if (!h || !base || !shape || !nd) throw eb::InvalidError("eb_exec_block: null argument");
+    std::vector<std::int64_t> b, s;
+    h->exec->local_block(k, b, s);
+    *nd = static_cast<int>(b.size());
+    std::copy(b.begin(), b.end(), base);
+    std::copy(s.begin(), s.end(), shape);
+  });
+}
+
+int eb_exec_stage_block(eb_exec* h, int k, const double* host_block) {
+  return exec_guard([&] {
+    if (!h || !host_block) throw eb::InvalidError("eb_exec_stage_block: null argument");
+    h->exec->stage_block(k, host_block);
+  });
+}
+
 int eb_exec_share_input(eb_exec* dst, int k_dst, eb_exec* src, int k_src) {
   return exec_guard([&] {
     if (!dst || !src) throw eb::InvalidError("eb_exec_share_input: null handle");
@@ -525,6 +543,40 @@ void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip) {
   if (skip > 0) gen.discard(static_cast<unsigned long long>(skip));
   for (int64_t k = 0; k < n; ++k)
     out[k] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0;
+}
+
+int eb_random_fill_block(double* out, uint64_t seed, int nd, const int64_t* gshape,
+                         const int64_t* base, const int64_t* shape) {
+  return eb::guard([&] {
+    if (nd < 1 || nd > 16 || !out || !gshape || !base || !shape)
+      throw eb::InvalidError("eb_random_fill_block: bad arguments");
+    for (int d = 0; d < nd; ++d)
+      if (shape[d] < 0 || base[d] < 0 || base[d] + shape[d] > gshape[d])
+        throw eb::InvalidError("eb_random_fill_block: block outside the tensor");
+    std::int64_t n = 1;
+    for (int d = 0; d < nd; ++d) n *= shape[d];
+    if (n == 0) return;
+    std::vector<std::int64_t> gstr(nd, 1);
+    for (int d = nd - 1; d > 0; --d) gstr[d - 1] = gstr[d] * gshape[d];
+    // walk the block's rows in stream order: skip the gap, draw the row
+    std::mt19937_64 gen(seed);
+    std::int64_t pos = 0;  // next stream index gen will produce
+    const std::int64_t run = shape[nd - 1];
+    std::vector<std::int64_t> idx(nd - 1, 0);
+    for (std::int64_t row = 0; row < n / run; ++row) {
+      std::int64_t off = base[nd - 1];
+      for (int d = 0; d + 1 < nd; ++d) off += (base[d] + idx[d]) * gstr[d];
+      if (off > pos) gen.discard(static_cast<unsigned long long>(off - pos));
+      double* o = out + row * run;
+      for (std::int64_t k = 0; k < run; ++k)
+        o[k] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0;
+      pos = off + run;
+      for (int d = nd - 2; d >= 0; --d) {
+        if (++idx[static_cast<std::size_t>(d)] < shape[d]) break;
+        idx[static_cast<std::size_t>(d)] = 0;
+      }
+    }
+  });
 }
 
 }  // extern "C"

@@ -393,6 +393,60 @@ void ScheduleExecutor::stage_inputs(const std::vector<const double*>& globals) {
   staged_ = true;
 }
 
+void ScheduleExecutor::local_block(int k, std::vector<std::int64_t>& base,
+                                   std::vector<std::int64_t>& shape) const {
+  if (owned_.size() != 1)
+    fail(errc::invalid_argument, "local_block: needs exactly one owned rank (one process per GPU)");
+  const std::string name = "in" + std::to_string(k);
+  bool found = false;
+  for (const TermPlan& term : pipe_.schedule.terms)
+    for (const AccessArray& arr : term.statement.arrays) {
+      if (arr.tensor != name) continue;
+      const TensorPlacement& place = term.placement_of(name);
+      const auto bc = place.block_coords_of(owned_[0]);
+      const auto b = place.dist.base_of(bc), s = place.dist.shape_of(bc);
+      if (found && (b != base || s != shape))
+        fail(errc::invalid_argument, "local_block: " + name + " is placed differently by two terms");
+      base = b;
+      shape = s;
+      found = true;
+    }
+  if (!found) fail(errc::invalid_argument, "local_block: no operand in" + std::to_string(k));
+}
+
+void ScheduleExecutor::stage_block(int k, const double* host_block) {
+  std::vector<std::int64_t> base, shape;
+  local_block(k, base, shape);
+  const std::string name = "in" + std::to_string(k);
+  const std::int64_t r = owned_[0];
+  for (const TermPlan& term : pipe_.schedule.terms)
+    for (const AccessArray& arr : term.statement.arrays) {
+      if (arr.tensor != name) continue;
+      const auto key = std::make_pair(term.index, name);
+      if (aliased_.count(key))
+        fail(errc::invalid_argument, "stage_block: " + name + " is shared from another executor");
+      auto it = inputs_.find(key);
+      if (it == inputs_.end()) {
+        std::vector<DevBlock> blocks(static_cast<std::size_t>(pipe_.schedule.procs));
+        DevBlock& b = blocks[static_cast<std::size_t>(r)];
+        b.base = base;
+        b.shape = shape;
+        b.ptr = input_arena_.alloc(prod(shape), stream_, false);
+        it = inputs_.emplace(key, std::move(blocks)).first;
+      }
+      const DevBlock& b = it->second[static_cast<std::size_t>(r)];
+      cuda_ok(cudaMemcpyAsync(b.ptr, host_block, static_cast<std::size_t>(prod(shape)) * 8,
+                              cudaMemcpyHostToDevice, stream_),
+              "H2D block");
+    }
+  // staged once every operand has device blocks on this rank
+  bool all = true;
+  for (const TermPlan& term : pipe_.schedule.terms)
+    for (const AccessArray& arr : term.statement.arrays)
+      if (arr.tensor.rfind("in", 0) == 0 && !inputs_.count({term.index, arr.tensor})) all = false;
+  staged_ = all;
+}
+
 void ScheduleExecutor::share_input(int k, const ScheduleExecutor& src, int k_src) {
   const std::string name = "in" + std::to_string(k), sname = "in" + std::to_string(k_src);
   if (!src.staged_) fail(errc::invalid_argument, "share_input: source executor not staged");

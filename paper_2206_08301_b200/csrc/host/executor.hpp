@@ -101,6 +101,11 @@ class ScheduleExecutor {
 
   // scatter (executor.cpp:48-65): every owned rank's input blocks to device.
   void stage_inputs(const std::vector<const double*>& global_inputs);
+  // One process = one rank: the box (global base, shape) of operand k this
+  // rank holds, and staging from a host buffer holding just that box — no
+  // process needs the global tensor (e.g. C5's 69 GB X at P = 8).
+  void local_block(int k, std::vector<std::int64_t>& base, std::vector<std::int64_t>& shape) const;
+  void stage_block(int k, const double* host_block);
   // Use another executor's staged device blocks for operand k (same tensor,
   // same placement on every owned rank): e.g. one X for the three MTTKRP
   // modes of a CP-ALS sweep.

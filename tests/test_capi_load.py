@@ -59,3 +59,17 @@ def test_reference_c_smoke_compiles_against_our_header(eb, tmp_path):
     subprocess.run(["gcc", "-std=c11", "-Wall", "-I", os.path.join(ROOT, "include"), REF_SMOKE,
                     "-L", libdir, "-leinplan_b200", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
     assert os.path.exists(exe)
+
+
+def test_random_block_is_the_box_of_random_tensor(eb):
+    """eb_random_fill_block: any box of random_tensor(shape, seed) without the
+    global tensor (multi-process staging of GB-scale inputs)."""
+    import numpy as np
+    import oracle
+    g = (6, 7, 9, 5)
+    full = oracle.random_tensor(g, 11)
+    for base, shape in [((0, 0, 0, 0), g), ((2, 3, 1, 0), (3, 4, 8, 5)), ((5, 6, 8, 4), (1, 1, 1, 1)),
+                        ((1, 0, 2, 1), (4, 7, 3, 2))]:
+        got = eb.random_block(11, g, base, shape)
+        want = full[tuple(slice(a, a + n) for a, n in zip(base, shape))]
+        assert np.array_equal(got, want)

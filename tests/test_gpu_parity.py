@@ -583,6 +583,25 @@ def test_share_input_across_modes(eb):
             check(ex.gather(), oracle.naive_evaluate(e, ext, ops))
 
 
+def test_stage_block_one_rank_process(eb):
+    """eb_exec_block / eb_exec_stage_block on a one-rank NCCL executor: the
+    rank's boxes generated with eb_random_fill_block (no global tensor) give
+    the same output as staging the global tensors."""
+    e, ext = "ijk,jb,kc->ibc", dict(i=24, j=40, k=32, b=8, c=6)
+    nid = eb.Executor.nccl_unique_id()
+    ex = eb.Executor(e, ext, 1, rank=0, nccl_id=nid)
+    ins = e.split("->")[0].split(",")
+    for k, t in enumerate(ins):
+        base, shape = ex.block(k)
+        gshape = [ext[c] for c in t]
+        assert base == [0] * len(t) and shape == gshape
+        ex.stage_block(k, eb.random_block(k, gshape, base, shape))
+    ex.run()
+    got = ex.gather()
+    want = oracle.naive_evaluate(e, ext, oracle.seeded_inputs(e, ext, 0))
+    check(got, want)
+
+
 def test_nccl_transport_single_rank(eb):
     """The one-process-per-GPU transport (NCCL communicator from a unique id,
     rank 0 of 1) runs the schedule and gathers on rank 0.  Multi-rank NCCL
