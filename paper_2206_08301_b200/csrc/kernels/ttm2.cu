@@ -314,13 +314,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 // sub-partition) each own 4 output rows and run step 1 on every published
 // stage; warp 12 issues the TMA boxes.  Per sub-partition per stage: 64 + 16
 // DMMAs, as before, but a slow warp no longer stalls the others.
-constexpr int kWsS0 = 8, kWsS1 = 4, kWsWarps = kWsS0 + kWsS1 + 1;
-constexpr int kWsStages = 6, kWsT0Slots = 2;
-constexpr int kWsT0Bytes = 2 * kK * kPlane;  // [j half][k][16 r][16 b]
-constexpr int kWsSmem = kWsStages * kXBytes + kWsT0Slots * kWsT0Bytes + 1024;
+// JP = j parts per k in step 0: 2 -> 8 step-0 warps (two per sub-partition,
+// j halves summed by step 1), 1 -> 4 step-0 warps each contracting all 64 j
+// (one step-0 and one step-1 warp per sub-partition, fewer non-DMMA
+// instructions per stage).
+template <int JP>
+struct WsCfg {
+  static constexpr int S0 = 4 * JP, S1 = 4, Warps = S0 + S1 + 1;
+  static constexpr int JW = kJ / JP, B16 = JW / 16;
+  static constexpr int Stages = 6, T0Slots = 2;
+  static constexpr int T0Bytes = JP * kK * kPlane;  // [j part][k][16 r][16 b]
+  static constexpr int Smem = Stages * kXBytes + T0Slots * T0Bytes + 1024;
+};
 
-__global__ void __launch_bounds__(kWsWarps * 32, 1)
+template <int JP>
+__global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     ttm2_ws_kernel(const __grid_constant__ CUtensorMap xmap, const Ttm2Params prm) {
+  using W = WsCfg<JP>;
+  constexpr int kWsS0 = W::S0, kWsS1 = W::S1, kWsStages = W::Stages, kWsT0Slots = W::T0Slots;
+  constexpr int kWsT0Bytes = W::T0Bytes;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_x[kWsStages];
   __shared__ __align__(8) uint64_t empty_x[kWsStages];
@@ -371,15 +383,15 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
 
   if (warp < kWsS0) {
     // ------------------------------------------------------------- step 0
-    const int kk = warp >> 1, jh = warp & 1;
-    double u1[2][4][2];
+    const int kk = warp / JP, jh = warp % JP;
+    double u1[W::B16][4][2];
 #pragma unroll
-    for (int b16 = 0; b16 < 2; ++b16)
+    for (int b16 = 0; b16 < W::B16; ++b16)
 #pragma unroll
       for (int s = 0; s < 4; ++s)
 #pragma unroll
         for (int nj = 0; nj < 2; ++nj) {
-          const int64_t j = 32 * jh + 16 * b16 + 2 * l + (s & 1) + 8 * (s >> 1);
+          const int64_t j = W::JW * jh + 16 * b16 + 2 * l + (s & 1) + 8 * (s >> 1);
           const int64_t n = 8 * nj + g;
           u1[b16][s][nj] = (j < prm.Q1 && n < prm.N1) ? __ldg(prm.U1 + j * prm.ldu1 + n) : 0.0;
         }
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
     uint32_t offa[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      const int j = 32 * jh + 2 * l + (s & 1) + 8 * (s >> 1);
+      const int j = W::JW * jh + 2 * l + (s & 1) + 8 * (s >> 1);
       offa[s] = (uint32_t)(kk * kJ + j) * 128u + (uint32_t)(g ^ (j & 7)) * 16u;
     }
     uint32_t offw[2][2];
@@ -414,7 +426,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
 #pragma unroll
           for (int nj = 0; nj < 2; ++nj) t[mi][nj][0] = t[mi][nj][1] = 0.0;
 #pragma unroll
-        for (int b16 = 0; b16 < 2; ++b16)
+        for (int b16 = 0; b16 < W::B16; ++b16)
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const double2 a2 = *reinterpret_cast<const double2*>(xs + offa[s] + b16 * 16 * 128);
@@ -479,9 +491,13 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
 #pragma unroll
       for (int ri = 0; ri < RW; ++ri)
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-          a[ri][mi] = *reinterpret_cast<const double*>(tb + offr[ri][mi]) +
-                      *reinterpret_cast<const double*>(tb + offr[ri][mi] + kK * kPlane);
+        for (int mi = 0; mi < 2; ++mi) {
+          double v = *reinterpret_cast<const double*>(tb + offr[ri][mi]);
+#pragma unroll
+          for (int q = 1; q < JP; ++q)  // the j-part partials, fixed order
+            v += *reinterpret_cast<const double*>(tb + offr[ri][mi] + q * kK * kPlane);
+          a[ri][mi] = v;
+        }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_t[ts]));
 #pragma unroll
@@ -545,15 +561,16 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
   count_launch();
 }
 
+template <int JP>
 void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    EB_CUDA(cudaFuncSetAttribute(ttm2_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kWsSmem));
+    EB_CUDA(cudaFuncSetAttribute(ttm2_ws_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 WsCfg<JP>::Smem));
     attr = true;
   }
   main_kernel_begin(st);
-  ttm2_ws_kernel<<<prm.G, kWsWarps * 32, kWsSmem, st>>>(xmap, prm);
+  ttm2_ws_kernel<JP><<<prm.G, WsCfg<JP>::Warps * 32, WsCfg<JP>::Smem, st>>>(xmap, prm);
   EB_CUDA(cudaGetLastError());
   main_kernel_end(st);
   count_launch();
@@ -595,8 +612,12 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
     pipe ? launch<16, true>(xmap, prm, st) : launch<16, false>(xmap, prm, st);
   else if (v && std::atoi(v) == 8)
     pipe ? launch<8, true>(xmap, prm, st) : launch<8, false>(xmap, prm, st);
-  else
-    launch_ws(xmap, prm, st);
+  else if (v && v[0] == 'w')
+    v[1] == '2' ? launch_ws<2>(xmap, prm, st) : launch_ws<1>(xmap, prm, st);
+  else if (prm.items >= 16 * (int64_t)prm.G)  // long streams per CTA: C5 term 0 1.555 -> 1.484 ms
+    launch_ws<1>(xmap, prm, st);
+  else  // few items per CTA (C5 term 1: 0.105 vs 0.112 ms)
+    launch_ws<2>(xmap, prm, st);
 }
 
 }  // namespace
