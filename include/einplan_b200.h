@@ -90,6 +90,17 @@ size_t eb_mttkrp2_workspace(const eb_contract_desc* d);
 int eb_mttkrp2(const eb_contract_desc* d, const double* A, int64_t lda, double* out1,
                void* workspace, size_t workspace_bytes, void* stream);
 
+/* One CP-ALS sweep of an order-3 tensor (not in the
+ * reference, which runs each MTTKRP as its own einsum): updates the factors
+ * A [I][R], B [J][R], C [K][R] (device, row-major) in place —
+ *   A = MTTKRP_0 ((B'B) (.) (C'C))^-1, B = MTTKRP_1 ((A'A) (.) (C'C))^-1,
+ *   C = MTTKRP_2 ((A'A) (.) (B'B))^-1, each with the factors already updated —
+ * with the dimension tree: T = X x_3 C is contracted once and serves modes 0
+ * and 1, so X is read twice per sweep, not three times.  R <= 64, K even. */
+size_t eb_cp3_als_workspace(int64_t I, int64_t J, int64_t K, int64_t R);
+int eb_cp3_als_sweep(const double* X, int64_t I, int64_t J, int64_t K, int64_t R, double* A,
+                     double* B, double* C, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fused TTM pair: the two TTM steps of one fused term with the intermediate
  * kept on chip (TTMc-O5 terms [t0,t1] and [t2,out]; replaces two
  * local_contract calls, proj/src/executor.cpp:220-235):

@@ -89,6 +89,25 @@ class Session:
         return st, _capi.take_string(p)
 
 
+def cp3_als_sweep(X, A, B, C, stream=None, workspace=None):
+    """One CP-ALS sweep (eb_cp3_als_sweep) on torch CUDA tensors: X [I][J][K],
+    factors [n][R], float64, contiguous; A, B, C are updated in place.
+    Returns the workspace tensor (reuse it across sweeps)."""
+    import torch
+    I, J, K = X.shape
+    R = A.shape[1]
+    L = _capi.lib()
+    nb = L.eb_cp3_als_workspace(I, J, K, R)
+    if nb == 0:
+        raise EinplanError(_capi.EINPLAN_E_INVALID, L.eb_last_error().decode())
+    if workspace is None or workspace.numel() < nb:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=X.device)
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _capi.check(L.eb_cp3_als_sweep(X.data_ptr(), I, J, K, R, A.data_ptr(), B.data_ptr(),
+                                   C.data_ptr(), workspace.data_ptr(), nb, s))
+    return workspace
+
+
 def random_block(seed: int, gshape, base, shape, out: np.ndarray | None = None) -> np.ndarray:
     """The box [base, base+shape) of random_tensor(gshape, seed), generated
     without materialising the global tensor (into `out` when given, e.g. a

@@ -183,9 +183,25 @@ __device__ __forceinline__ void fold_krp(double (&t)[MI][NT][2], double (&m)[MI]
 // element e of tiles (2q, 2q+1) are columns 16q + 4l + 2e + {0, 1}.
 __device__ __forceinline__ int vc_row(int i, int g) { return 16 * (i >> 1) + 2 * g + (i & 1); }
 
-template <int MI, int NT, int MT, int WM, int SPL, bool VC = false>
+template <int MI, int NT, int MT, int WM, int SPL, bool VC = false, bool DIR = false>
 __device__ __forceinline__ void flush_partial(double (&acc)[MI][NT][2], const ContractParams& prm,
-                                              int sg, int wm, int split, int g, int l) {
+                                              int sg, int wm, int split, int g, int l,
+                                              int64_t mt = 0) {
+  if constexpr (DIR) {  // whole row tile in this CTA: final values, out[m][col0 + n]
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int64_t row = mt * MT + wm * WM + (VC ? vc_row(i, g) : i * 8 + g);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = VC ? 16 * (j >> 1) + 4 * l + 2 * e + (j & 1) : j * 8 + 2 * l + e;
+          if (row < prm.M && prm.col0 + c < prm.R) prm.out[row * prm.ldo + prm.col0 + c] = acc[i][j][e];
+          acc[i][j][e] = 0.0;
+        }
+      }
+    return;
+  }
   double* dst = prm.out +
                 (((int64_t)blockIdx.x * prm.segmax + sg) * SPL + split) * (int64_t)MT * (NT * 8);
   if constexpr (VC) {
@@ -267,7 +283,8 @@ __device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
 // then M += KRP[o] (.) T once per outer index — the Khatri-Rao product is a
 // per-column scale of T and is never formed.  One partial per k-split group.
 // BATCHED (TTM) requires KS == 1 and writes each (row tile, o) unit once.
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
+          bool DIR = false>
 __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
@@ -304,8 +321,12 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   }
   __syncthreads();
 
-  const int64_t i0 = (int64_t)blockIdx.x * prm.items / prm.G;
-  const int64_t i1 = (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
+  const int64_t per_tile_items = prm.O * prm.KC;
+  const int64_t mtiles_all = prm.items / per_tile_items;
+  const int64_t i0 = DIR ? ((int64_t)blockIdx.x * mtiles_all / prm.G) * per_tile_items
+                        : (int64_t)blockIdx.x * prm.items / prm.G;
+  const int64_t i1 = DIR ? ((int64_t)(blockIdx.x + 1) * mtiles_all / prm.G) * per_tile_items
+                        : (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
 
   if (warp == NCW) {
     // ------------------------------------------------------------ producer
@@ -568,7 +589,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
         fold_krp<MI, NT>(acc, macc, krow);
       }
       if (mt != cur_mt) {
-        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL, VC>(macc, prm, seg, wm, ks + KS * os, g, l);
+        if (cur_mt >= 0) flush_partial<MI, NT, MT, WM, SPL, VC, DIR>(macc, prm, seg, wm, ks + KS * os, g, l, cur_mt);
         ++seg;
         cur_mt = mt;
       }
@@ -740,7 +761,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
       if constexpr (TWO)
         emit_two<MI, NT, NWM, MT, WM>(acc, red2, prm, cur_mt, cur_o, o_kc0, n_emit++, wm, g, l, lane);
       fold_krp<MI, NT>(acc, macc, krow);
-      flush_partial<MI, NT, MT, WM, SPL, VC>(macc, prm, seg, wm, ks + KS * os, g, l);
+      flush_partial<MI, NT, MT, WM, SPL, VC, DIR>(macc, prm, seg, wm, ks + KS * os, g, l, cur_mt);
     }
   }
 }
@@ -880,6 +901,10 @@ struct Plan {
   int64_t kin = 0, O = 0, KC = 0, mtiles = 0, items = 0;
   int G = 0, segmax = 0;
   int chunks = 1;      // rank-column chunks of <= 64
+  // REDUCE over many row tiles with no outer index (e.g. T = X x3 C: 8192
+  // tiles): CTAs take whole row tiles (ranges aligned to tiles) and write
+  // out[m][col0 + n] directly — no partial slots, no reduction kernel
+  bool direct = false;
   size_t u_bytes = 0;  // staged factor buffer (per chunk)
   size_t ws_bytes = 0; // partial slots (per chunk)
 };
@@ -944,13 +969,15 @@ Plan plan_of(const eb_contract_desc* d) {
     p.items = p.mtiles * p.O * p.KC;
     p.G = (int)std::min<int64_t>(p.items, (int64_t)sms);
     const int64_t per_tile = p.O * p.KC;
+    p.direct = !p.col && p.nwm == 8 && p.ks == 1 && p.O == 1 && p.mtiles >= 16 * (int64_t)sms;
     int segmax = 1;
     for (int c = 0; c < p.G; ++c) {
       const int64_t c0 = (int64_t)c * p.items / p.G, c1 = (int64_t)(c + 1) * p.items / p.G;
       if (c1 > c0) segmax = std::max<int>(segmax, (int)((c1 - 1) / per_tile - c0 / per_tile + 1));
     }
     p.segmax = segmax;
-    p.ws_bytes = (size_t)p.G * segmax * p.ks * p.os * p.mt * (p.nt * 8) * sizeof(double);
+    p.ws_bytes = p.direct ? 0
+                          : (size_t)p.G * segmax * p.ks * p.os * p.mt * (p.nt * 8) * sizeof(double);
   }
   if (p.col) {
     p.u_bytes = (size_t)d->Q * ((d->R + 15) / 16 * 16) * sizeof(double);
@@ -962,11 +989,12 @@ Plan plan_of(const eb_contract_desc* d) {
   return p;
 }
 
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
+          bool DIR = false>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
   using T = Tile<COL, NWM * WM, NT, KD, OS>;
-  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR>;
   static bool attr = false;
   if (!attr) {
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
@@ -996,6 +1024,18 @@ template <bool COL>
 void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                      const ContractParams& prm, cudaStream_t st) {
   if (p.os == 2) return dispatch_nt<COL, false, 4, 16, 1, 64, 2, 1, 8>(nt, xm, um, prm, st);
+  if constexpr (!COL) {
+    if (p.direct) {
+      switch (nt) {
+#define EB_DIR_CASE(N) \
+  case N: return launch_t<false, false, 8, 16, 1, 32, 1, N, false, true>(xm, um, prm, st);
+        EB_DIR_CASE(1) EB_DIR_CASE(2) EB_DIR_CASE(3) EB_DIR_CASE(4)
+        EB_DIR_CASE(5) EB_DIR_CASE(6) EB_DIR_CASE(7) EB_DIR_CASE(8)
+#undef EB_DIR_CASE
+        default: throw InvalidError("eb_contract: unsupported column tile count");
+      }
+    }
+  }
   if (p.ks == 1) return dispatch_nt<COL, false, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
   return dispatch_nt<COL, false, 4, 16, 2, 32, 1, 1, 8>(nt, xm, um, prm, st);
 }
@@ -1113,10 +1153,10 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
       umap = umap_col;
     }
     ContractParams q = prm;
-    q.out = p.batched ? d->out : part;
+    q.out = (p.batched || p.direct) ? d->out : part;
     q.ldo = d->R;
     launch_variant(p, nt, xmap, umap, q, st);
-    if (!p.batched) {
+    if (!p.batched && !p.direct) {
       const int np = nt * 8;
       launch_reduce(part, d->out, d->M, (int)d->R, col0, d->R, np, p.mt, p.ks * p.os, p.O * p.KC,
                     p.items, p.G, p.segmax, st);
@@ -1140,6 +1180,10 @@ size_t two_slot_bytes(const Plan& p) {
 Plan two_plan(const eb_contract_desc* d) {
   Plan p = plan_of(d);
   check_two(d, p);
+  if (p.direct) {  // the pair keeps the partial-slot scheme
+    p.direct = false;
+    p.ws_bytes = (size_t)p.G * p.segmax * p.mt * (p.nt * 8) * sizeof(double);
+  }
   // every outer index may span at most two CTAs (slot h = 0 / 1)
   if (p.items / p.G < p.KC) {
     p.G = (int)std::max<int64_t>(1, p.items / p.KC);

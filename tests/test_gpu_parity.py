@@ -286,6 +286,36 @@ def test_exec_run_pair_falls_back_when_not_shared(eb):
     check(ex1.gather(), oracle.naive_evaluate("ijk,ia,ka->ja", ext, [X, F["i"], F["k"]]))
 
 
+def _np_als_sweep(X, A, B, C):
+    """One CP-ALS sweep in numpy (float64): the textbook update order."""
+    A = np.einsum("ijk,jr,kr->ir", X, B, C) @ np.linalg.inv((B.T @ B) * (C.T @ C))
+    B = np.einsum("ijk,ir,kr->jr", X, A, C) @ np.linalg.inv((A.T @ A) * (C.T @ C))
+    C = np.einsum("ijk,ir,jr->kr", X, A, B) @ np.linalg.inv((A.T @ A) * (B.T @ B))
+    return A, B, C
+
+
+@pytest.mark.parametrize("I,J,K,R", [(40, 36, 50, 8), (130, 20, 34, 16), (64, 64, 64, 32),
+                                     (257, 3, 6, 4), (300, 40, 18, 24),
+                                     (600, 512, 16, 8)])  # T on the direct (tile-aligned) path
+def test_cp3_als_sweep(eb, I, J, K, R):
+    """eb_cp3_als_sweep (dimension tree: T = X x3 C shared by modes 0 and 1,
+    Gram/Hadamard/Cholesky solves on the device) = the numpy sweep, twice."""
+    torch = _torch()
+    rng = np.random.default_rng(I + J + K + R)
+    X = rng.uniform(-1, 1, (I, J, K))
+    F = [rng.uniform(-1, 1, (n, R)) for n in (I, J, K)]
+    g = [torch.from_numpy(a.copy()).cuda() for a in [X] + F]
+    ws = None
+    want = F
+    for _ in range(2):
+        ws = eb.cp3_als_sweep(g[0], g[1], g[2], g[3], workspace=ws)
+        want = _np_als_sweep(X, *want)
+    torch.cuda.synchronize()
+    for got, w in zip(g[1:], want):
+        rel = np.linalg.norm(got.cpu().numpy() - w) / np.linalg.norm(w)
+        assert rel <= 1e-9, rel
+
+
 def test_contract_order5_all_krp_rows(eb):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
