@@ -560,6 +560,7 @@ def main():
             "kernel": "eb::contract_kernel (FP64 DMMA.8x8x4, TMA SWIZZLE_128B ring)",
             "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.jsonl "
                            "(MEASURED_PEAKS.json has no FP64 figure)",
+            "fp64_achieved_tflops": achieved,
             "kernel_ms_per_launch": kern_ms, "kernel_launches_timed": kn.value,
             "kernel_share_of_step": kms.value / max(ms, 1e-9),
             "hbm_achieved_gbs": _x_bytes(modes, P) * (2.0 / 3.0 if dimtree else 1.0)
@@ -567,6 +568,26 @@ def main():
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
             "algorithmic_flops_per_launch": per_launch_flops,
             "launches_per_step": launches_per_step}
+    if args.config == "C5":
+        # C5 sits at the HBM side of the ridge (1.316 ms of HBM vs
+        # 1.233 ms of FP64 per GPU): the binding roof is bandwidth.  Bytes the
+        # two eb_ttm2 launches must move per step: X, the term-0 output t1
+        # written and read back, the output.
+        e0, ext0, _ = modes[0]
+        x_el = int(np.prod([ext0[c] for c in e0.split("->")[0].split(",")[0]])) // P
+        t1_el = x_el // (ext0["j"] * ext0["k"]) * ext0["b"] * ext0["c"]
+        out_el = x_el // (ext0["j"] * ext0["k"] * ext0["l"] * ext0["m"]) * \
+            ext0["b"] * ext0["c"] * ext0["d"] * ext0["e"]
+        kbytes = 8.0 * (x_el + 2 * t1_el + out_el)
+        gbs = kbytes / (kms.value / args.steps * 1e-3) / 1e9
+        hbm_peak = float(peaks.get("hbm_gbs") or 6650.0)
+        roof.update({"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": gbs / hbm_peak,
+                     "kernel": "eb::ttm2_ws_kernel (two fused TTM pairs, FP64 DMMA)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy test)" if peaks.get("hbm_gbs")
+                                    else "fallback (B200_PROFILING.md)",
+                     "algorithmic_bytes_per_step": kbytes,
+                     "hbm_achieved_gbs": gbs})
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
