@@ -40,6 +40,7 @@
 #include "../host/status.hpp"
 #include "device_common.cuh"
 #include "tma_host.hpp"
+#include "rf.hpp"
 #include "einplan_b200.h"
 
 namespace eb {
@@ -1054,6 +1055,8 @@ void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensor
 void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStream_t st) {
   check_device();
   const Plan p = plan_of(d);
+  // short contracted mode, few rows (order-5 mode 0): U resident in registers
+  if (rf_run(d, ws, ws_bytes, st)) return;
   const size_t need = (p.u_bytes + p.ws_bytes);
   if (ws_bytes < need) throw InvalidError("eb_contract: workspace too small");
   uint8_t* wsb = static_cast<uint8_t*>(ws);
@@ -1301,7 +1304,7 @@ extern "C" int eb_mttkrp2(const eb_contract_desc* d, const double* a, int64_t ld
 extern "C" size_t eb_contract_workspace(const eb_contract_desc* d) {
   try {
     eb::Plan p = eb::plan_of(d);
-    return p.u_bytes + p.ws_bytes;
+    return std::max(p.u_bytes + p.ws_bytes, eb::rf_workspace(d));
   } catch (const std::exception& e) {
     eb::set_error(e.what());
     return 0;

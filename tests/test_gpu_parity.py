@@ -329,6 +329,37 @@ def test_contract_order5_all_krp_rows(eb):
     check(got, want)
 
 
+RF_CASES = [  # (einsum, extents, P, M, Q, L, #pre, #mid): the resident-factor path
+    ("ijklm,ja,ka,la,ma->ia", dict(i=40, j=6, k=7, l=5, m=64, a=24), 1, 40, 210, 64, 0, 3),
+    ("ijkl,ja,ka,la->ia", dict(i=100, j=9, k=4, l=32, a=16), 1, 100, 36, 32, 0, 2),
+    ("ijk,ia,ka->ja", dict(i=13, j=50, k=48, a=5), 13, 50, 1, 48, 1, 0),
+    ("ijkl,ia,ka,la->ja", dict(i=7, j=64, k=11, l=16, a=20), 7, 64, 11, 16, 1, 1),
+    ("ijk,ja,ka->ia", dict(i=1, j=300, k=64, a=24), 1, 1, 300, 64, 0, 1),
+]
+
+
+@pytest.mark.parametrize("case", range(len(RF_CASES)))
+@pytest.mark.parametrize("knob", ["", "EB_RF_MI=2", "EB_NO_RF=1"])
+def test_contract_resident_factor_path(eb, case, knob, monkeypatch):
+    """Short contracted mode (L <= 64, L % 16 == 0), R <= 24, M < 128: the
+    resident-factor kernel (mttkrp_rf.cu; 8 x 8-row or 4 x 16-row consumer
+    warps) and, with EB_NO_RF, the general kernel — both against the oracle."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    e, ext, P, M, Q, L, npre, nmid = RF_CASES[case]
+    if knob:
+        k, v = knob.split("=")
+        monkeypatch.setenv(k, v)
+    ops = oracle.seeded_inputs(e, ext, 31 + case)
+    want = oracle.naive_evaluate(e, ext, ops)
+    g = [torch.from_numpy(o).cuda() for o in ops]
+    facs = g[1:-1]
+    out = torch.zeros(want.shape, dtype=torch.float64, device="cuda")
+    got = _contract(eb, C.EB_ROW, C.EB_REDUCE, P, M, Q, L, ext["a"], g[0], g[-1], facs[:npre],
+                    facs[npre:npre + nmid], out)
+    check(got, want)
+
+
 # ------------------------------------------------------- executor / C ABI --
 
 @pytest.mark.parametrize("name,einsum,ext", DESK, ids=[d[0] for d in DESK])
