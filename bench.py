@@ -557,7 +557,9 @@ def main():
     traffic = _traffic(args.config)
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-            "kernel": "eb::contract_kernel (FP64 DMMA.8x8x4, TMA SWIZZLE_128B ring)",
+            "kernel": ("eb::mttkrp_rf_kernel (U resident in registers, FP64 DMMA.8x8x4, "
+                       "16 rows x 8 outer indices per TMA stage)" if args.config == "C3" else
+                       "eb::contract_kernel (FP64 DMMA.8x8x4, TMA SWIZZLE_128B ring)"),
             "peak_source": "measured FP64 DMMA peak, profiles/fp64_peak_r01.jsonl "
                            "(MEASURED_PEAKS.json has no FP64 figure)",
             "fp64_achieved_tflops": achieved,

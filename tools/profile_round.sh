@@ -10,10 +10,12 @@ NCU="ncu --clock-control none"
 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_bench.log 2>&1
 # 2) full captures of the dominant kernel per configuration
-for c in c2m0 c2m2 c2pair c1 c3; do
+for c in c2m0 c2m2 c2pair c1; do
   timeout 600 $NCU --set full --import-source on -k regex:contract_kernel -c 1 -o $O/ncu_$c \
     python tools/prof_contract.py $c 2 > $O/ncu_$c.log 2>&1
 done
+timeout 600 $NCU --set full --import-source on -k regex:mttkrp_rf -c 1 -o $O/ncu_c3 \
+  python tools/prof_contract.py c3 2 > $O/ncu_c3.log 2>&1
 timeout 600 $NCU --set full --import-source on -k regex:ttm2 -c 2 -o $O/ncu_c5_ttm2 \
   python tools/ttm2_bench.py 1 > $O/ncu_c5.log 2>&1
 timeout 900 $NCU --set full --import-source on -k regex:contract_kernel -c 2 -o $O/ncu_c4 \
