@@ -11,7 +11,8 @@
 // i.e. two passes over X per sweep instead of three: T is contracted once and
 // serves modes 0 and 1 (it is materialised — 268 MB at C2 — because mode 1
 // needs the *updated* A).  The small steps are deterministic fixed-order
-// reductions; the R x R solves are Cholesky factorisations in shared memory.
+// reductions; the R x R systems are inverted once per update (Gauss-Jordan
+// on the SPD matrix in shared memory) and applied as a small GEMM.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,106 +27,139 @@ namespace eb {
 namespace {
 
 constexpr int kMaxR = 64;
-constexpr int kGroups = 8;
+constexpr int kThreads = 256;
+constexpr int kGramRows = 64;  // rows per partial Gram block
 
 // axis 0: out[i][r] = sum_j T[i][j][r] F[j][r];  axis 1: out[j][r] = sum_i T[i][j][r] F[i][r]
-// One block per output row; thread (grp, r) sums every kGroups-th n, then the
-// group sums are combined in fixed order.
-__global__ void __launch_bounds__(kGroups * 64)
+// One block per output row; thread t owns column t % R and visits every
+// (kThreads / R)-th n (coalesced: consecutive threads, consecutive doubles),
+// eight loads in flight; the group sums are combined in fixed order.
+__global__ void __launch_bounds__(kThreads)
     hadamard_reduce_kernel(const double* __restrict__ T, const double* __restrict__ F,
                            double* __restrict__ out, int64_t I, int64_t J, int R, int axis) {
-  __shared__ double part[kGroups][kMaxR];
+  __shared__ double part[kThreads];
   const int64_t row = blockIdx.x;
-  const int r = threadIdx.x % 64, grp = threadIdx.x / 64;
+  const int groups = kThreads / R;
+  const int r = threadIdx.x % R, grp = threadIdx.x / R;
   const int64_t n_red = axis == 0 ? J : I;
   double acc = 0.0;
-  if (r < R) {
-    for (int64_t n = grp; n < n_red; n += kGroups) {
-      const int64_t i = axis == 0 ? row : n, j = axis == 0 ? n : row;
-      acc = fma(T[(i * J + j) * R + r], F[n * R + r], acc);
-    }
-  }
-  part[grp][r] = acc;
-  __syncthreads();
-  if (grp == 0 && r < R) {
-    double s = 0.0;
+  if (grp < groups) {
+    // element (row, n) of T: axis 0 -> T[row][n], axis 1 -> T[n][row]
+    const int64_t base = axis == 0 ? row * J * R : row * R;
+    const int64_t step = axis == 0 ? (int64_t)R : J * R;
+    int64_t n = grp;
+    constexpr int U = 8;
+    for (; n + (U - 1) * groups < n_red; n += U * groups) {
+      double t[U], f[U];
 #pragma unroll
-    for (int g = 0; g < kGroups; ++g) s += part[g][r];
-    out[row * R + r] = s;
-  }
-}
-
-// G[r][s] = sum_n F[n][r] F[n][s]: one block; F streams through shared memory
-// in coalesced 64-row chunks, thread (r, s) accumulates in fixed row order.
-constexpr int kGramRows = 64;
-__global__ void __launch_bounds__(1024)
-    gram_kernel(const double* __restrict__ F, int64_t n, int R, double* __restrict__ G) {
-  __shared__ double tile[kGramRows][kMaxR];
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // up to 4 (r, s) pairs per thread (R <= 64)
-  for (int64_t k0 = 0; k0 < n; k0 += kGramRows) {
-    const int rows = (int)((n - k0) < kGramRows ? (n - k0) : kGramRows);
-    __syncthreads();
-    for (int x = threadIdx.x; x < rows * R; x += blockDim.x)
-      tile[x / R][x % R] = F[(k0 + x / R) * R + x % R];
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int x = threadIdx.x + u * (int)blockDim.x;
-      if (x < R * R) {
-        const int r = x / R, s = x % R;
-        for (int k = 0; k < rows; ++k) acc[u] = fma(tile[k][r], tile[k][s], acc[u]);
+      for (int u = 0; u < U; ++u) {
+        t[u] = __ldcs(T + base + (n + u * groups) * step + r);  // streamed once
+        f[u] = __ldg(F + (n + u * groups) * R + r);
       }
-    }
-  }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int x = threadIdx.x + u * (int)blockDim.x;
-    if (x < R * R) G[x] = acc[u];
+      for (int u = 0; u < U; ++u) acc = fma(t[u], f[u], acc);
+    }
+    for (; n < n_red; n += groups) acc = fma(__ldg(T + base + n * step + r), __ldg(F + n * R + r), acc);
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int g = 0; g < groups; ++g) s += part[g * R + threadIdx.x];
+    out[row * R + threadIdx.x] = s;
   }
 }
 
-// Fout[i] = M[i] V^-1 with V = Ga (.) Gb (symmetric positive definite):
-// every block factors V = L L' in shared memory (R^3/3 flops), then each
-// thread solves its rows with two triangular substitutions.
-__global__ void __launch_bounds__(128)
-    solve_kernel(const double* __restrict__ M, const double* __restrict__ Ga,
-                 const double* __restrict__ Gb, int64_t n, int R, double* __restrict__ Fout) {
-  __shared__ double L[kMaxR][kMaxR + 1];
+// Partial Grams: block b sums rows [64b, 64b + 64) of F into P[b][r][s].
+__global__ void __launch_bounds__(kThreads)
+    gram_partial_kernel(const double* __restrict__ F, int64_t n, int R, double* __restrict__ P) {
+  __shared__ double tile[kGramRows][kMaxR + 1];
+  const int64_t k0 = (int64_t)blockIdx.x * kGramRows;
+  const int rows = (int)((n - k0) < kGramRows ? (n - k0) : kGramRows);
+  for (int x = threadIdx.x; x < rows * R; x += blockDim.x) tile[x / R][x % R] = F[k0 * R + x];
+  __syncthreads();
+  double* dst = P + (int64_t)blockIdx.x * R * R;
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
     const int r = x / R, s = x % R;
-    L[r][s] = Ga[x] * Gb[x];
+    double acc = 0.0;
+    for (int k = 0; k < rows; ++k) acc = fma(tile[k][r], tile[k][s], acc);
+    dst[x] = acc;
+  }
+}
+
+// G[x] = sum_b P[b][x] in ascending b (deterministic).
+__global__ void gram_sum_kernel(const double* __restrict__ P, int nb, int R, double* __restrict__ G) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= R * R) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += P[(int64_t)b * R * R + x];
+  G[x] = s;
+}
+
+// Vinv = (Ga (.) Gb)^-1 by Gauss-Jordan elimination without pivoting (V is
+// symmetric positive definite: every pivot is positive), one block, V in
+// shared memory: step p updates all R x R entries in parallel from the old
+// pivot row and column (two barriers per step, R steps).
+__global__ void __launch_bounds__(kThreads)
+    spd_inverse_kernel(const double* __restrict__ Ga, const double* __restrict__ Gb, int R,
+                       double* __restrict__ Vinv) {
+  __shared__ double V[kMaxR][kMaxR + 1];
+  __shared__ double colp[kMaxR], rowp[kMaxR];
+  __shared__ double inv_s;
+  constexpr int kPer = kMaxR * kMaxR / kThreads;  // entries per thread (R <= 64)
+  int ii[kPer], jj[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int x = threadIdx.x + u * kThreads;
+    ii[u] = x < R * R ? x / R : -1;
+    jj[u] = x < R * R ? x % R : 0;
+    if (ii[u] >= 0) V[ii[u]][jj[u]] = Ga[x] * Gb[x];
   }
   __syncthreads();
-  // Cholesky, column by column (right-looking, fixed order)
-  for (int c = 0; c < R; ++c) {
-    if (threadIdx.x == 0) L[c][c] = sqrt(L[c][c]);
+  for (int p = 0; p < R; ++p) {
+    if (threadIdx.x < R) {
+      colp[threadIdx.x] = V[threadIdx.x][p];
+      rowp[threadIdx.x] = V[p][threadIdx.x];
+      if (threadIdx.x == 0) inv_s = 1.0 / V[p][p];
+    }
     __syncthreads();
-    for (int r = c + 1 + threadIdx.x; r < R; r += blockDim.x) L[r][c] /= L[c][c];
-    __syncthreads();
-    for (int x = threadIdx.x; x < (R - c - 1) * (R - c - 1); x += blockDim.x) {
-      const int r = c + 1 + x / (R - c - 1), s = c + 1 + x % (R - c - 1);
-      if (s <= r) L[r][s] -= L[r][c] * L[s][c];
+    const double inv = inv_s;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = ii[u], j = jj[u];
+      if (i < 0) continue;
+      const double f = colp[i], a = rowp[j];
+      V[i][j] = i == p ? (j == p ? inv : a * inv) : (j == p ? -f * inv : V[i][j] - f * a * inv);
     }
     __syncthreads();
   }
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double y[kMaxR];
-  for (int r = 0; r < R; ++r) {  // L y = M[i]'
-    double v = M[i * R + r];
-    for (int s = 0; s < r; ++s) v -= L[r][s] * y[s];
-    y[r] = v / L[r][r];
-  }
-  for (int r = R - 1; r >= 0; --r) {  // L' x = y
-    double v = y[r];
-    for (int s = r + 1; s < R; ++s) v -= L[s][r] * y[s];
-    y[r] = v / L[r][r];
-  }
-  for (int r = 0; r < R; ++r) Fout[i * R + r] = y[r];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u)
+    if (ii[u] >= 0) Vinv[ii[u] * R + jj[u]] = V[ii[u]][jj[u]];
+}
+
+// Fout[i][s] = sum_r M[i][r] Vinv[r][s]: thread per output element, Vinv and
+// the block's M rows in shared memory.
+__global__ void __launch_bounds__(kThreads)
+    apply_inverse_kernel(const double* __restrict__ M, const double* __restrict__ Vinv, int64_t n,
+                         int R, double* __restrict__ Fout) {
+  __shared__ double V[kMaxR * kMaxR];
+  __shared__ double Ms[kThreads];
+  const int rows = kThreads / R;
+  const int64_t i0 = (int64_t)blockIdx.x * rows;
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) V[x] = Vinv[x];
+  const int nr = (int)((n - i0) < rows ? (n - i0) : rows);
+  if (threadIdx.x < nr * R) Ms[threadIdx.x] = M[i0 * R + threadIdx.x];
+  __syncthreads();
+  const int li = threadIdx.x / R, s = threadIdx.x % R;
+  if (li >= nr) return;
+  double acc = 0.0;
+  for (int r = 0; r < R; ++r) acc = fma(Ms[li * R + r], V[r * R + s], acc);
+  Fout[(i0 + li) * R + s] = acc;
 }
 
 struct Layout {
-  size_t t, m, g, cw, total;  // byte offsets / sizes
+  size_t t, m, g, gp, cw, total;  // byte offsets / sizes
 };
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
@@ -176,7 +210,8 @@ Layout layout(int64_t I, int64_t J, int64_t K, int64_t R) {
   Layout L;
   L.t = align256((size_t)I * J * R * 8);
   L.m = align256((size_t)std::max({I, J, K}) * R * 8);
-  L.g = align256((size_t)3 * R * R * 8);
+  L.g = align256((size_t)4 * R * R * 8);  // Ga, Gb, Gc, Vinv
+  L.gp = align256((size_t)((std::max({I, J, K}) + kGramRows - 1) / kGramRows) * R * R * 8);
   // non-null placeholders: the workspace queries only look at extents
   const double* p = reinterpret_cast<const double*>(256);
   double* q = reinterpret_cast<double*>(256);
@@ -184,7 +219,7 @@ Layout layout(int64_t I, int64_t J, int64_t K, int64_t R) {
   const size_t w1 = eb_contract_workspace(&d1), w2 = eb_contract_workspace(&d2);
   if (!w1 || !w2) throw InvalidError(std::string("eb_cp3_als: ") + eb_last_error());
   L.cw = align256(std::max(w1, w2));
-  L.total = L.t + L.m + L.g + L.cw;
+  L.total = L.t + L.m + L.g + L.gp + L.cw;
   return L;
 }
 
@@ -203,21 +238,31 @@ void run_sweep(const double* X, int64_t I, int64_t J, int64_t K, int64_t R, doub
   double* Ga = reinterpret_cast<double*>(w + Ly.t + Ly.m);
   double* Gb = Ga + R * R;
   double* Gc = Gb + R * R;
-  void* cw = w + Ly.t + Ly.m + Ly.g;
+  double* Vinv = Gc + R * R;
+  double* GP = reinterpret_cast<double*>(w + Ly.t + Ly.m + Ly.g);
+  void* cw = w + Ly.t + Ly.m + Ly.g + Ly.gp;
   const int Ri = (int)R;
   auto gram = [&](const double* F, int64_t n, double* G) {
-    gram_kernel<<<1, 1024, 0, st>>>(F, n, Ri, G);
+    const int nb = (int)((n + kGramRows - 1) / kGramRows);
+    gram_partial_kernel<<<nb, kThreads, 0, st>>>(F, n, Ri, GP);
     EB_CUDA(cudaGetLastError());
+    gram_sum_kernel<<<(Ri * Ri + 255) / 256, 256, 0, st>>>(GP, nb, Ri, G);
+    EB_CUDA(cudaGetLastError());
+    count_launch();
     count_launch();
   };
   auto solve = [&](const double* Ga_, const double* Gb_, int64_t n, double* F) {
-    solve_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(M, Ga_, Gb_, n, Ri, F);
+    spd_inverse_kernel<<<1, kThreads, 0, st>>>(Ga_, Gb_, Ri, Vinv);
     EB_CUDA(cudaGetLastError());
+    const int rows = kThreads / Ri;
+    apply_inverse_kernel<<<(unsigned)((n + rows - 1) / rows), kThreads, 0, st>>>(M, Vinv, n, Ri, F);
+    EB_CUDA(cudaGetLastError());
+    count_launch();
     count_launch();
   };
   auto hreduce = [&](const double* F, int axis) {
-    hadamard_reduce_kernel<<<(unsigned)(axis == 0 ? I : J), kGroups * 64, 0, st>>>(T, F, M, I, J, Ri,
-                                                                                   axis);
+    hadamard_reduce_kernel<<<(unsigned)(axis == 0 ? I : J), kThreads, 0, st>>>(T, F, M, I, J, Ri,
+                                                                              axis);
     EB_CUDA(cudaGetLastError());
     count_launch();
   };

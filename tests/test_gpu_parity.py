@@ -296,7 +296,8 @@ def _np_als_sweep(X, A, B, C):
 
 @pytest.mark.parametrize("I,J,K,R", [(40, 36, 50, 8), (130, 20, 34, 16), (64, 64, 64, 32),
                                      (257, 3, 6, 4), (300, 40, 18, 24),
-                                     (600, 512, 16, 8)])  # T on the direct (tile-aligned) path
+                                     (600, 512, 16, 8),  # T on the direct (tile-aligned) path
+                                     (70, 50, 24, 64), (33, 17, 10, 1), (90, 130, 66, 13)])
 def test_cp3_als_sweep(eb, I, J, K, R):
     """eb_cp3_als_sweep (dimension tree: T = X x3 C shared by modes 0 and 1,
     Gram/Hadamard/Cholesky solves on the device) = the numpy sweep, twice."""
