@@ -691,7 +691,7 @@ def _h2d_gbs(nbytes):
 
 def _time_cp_als(eb, inputs, stream, args, flops_tree):
     """A full CP-ALS sweep (eb_cp3_als_sweep: the three MTTKRPs plus the
-    Gram / Hadamard / Cholesky updates, dimension tree) on the C2 tensor,
+    Gram / Hadamard / SPD-inverse updates, dimension tree) on the C2 tensor,
     X resident; timed like the headline."""
     import torch
     X = torch.from_numpy(inputs[0][0]).to("cuda", non_blocking=False)
@@ -716,7 +716,7 @@ def _time_cp_als(eb, inputs, stream, args, flops_tree):
     torch.cuda.empty_cache()
     return {"ms_per_sweep": ms, "mttkrp_gflops": flops_tree / (ms * 1e-3) / 1e9,
             "factors_finite": finite,
-            "note": "one CP-ALS sweep (3 MTTKRPs + Gram/Hadamard/Cholesky updates) with the "
+            "note": "one CP-ALS sweep (3 MTTKRPs + Gram/Hadamard/SPD-inverse updates) with the "
                     "dimension tree: 2 passes over X; value counts the 3 reference MTTKRP trees"}
 
 

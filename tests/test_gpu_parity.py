@@ -300,7 +300,7 @@ def _np_als_sweep(X, A, B, C):
                                      (70, 50, 24, 64), (33, 17, 10, 1), (90, 130, 66, 13)])
 def test_cp3_als_sweep(eb, I, J, K, R):
     """eb_cp3_als_sweep (dimension tree: T = X x3 C shared by modes 0 and 1,
-    Gram/Hadamard/Cholesky solves on the device) = the numpy sweep, twice."""
+    Gram/Hadamard/SPD-inverse updates on the device) = the numpy sweep, twice."""
     torch = _torch()
     rng = np.random.default_rng(I + J + K + R)
     X = rng.uniform(-1, 1, (I, J, K))
