@@ -379,6 +379,21 @@ def test_run_json_desk_kernels(eb, name, einsum, ext, P):
     check(got, want)
 
 
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_run_json_order5_resident_factor_blocks(eb, P):
+    """Order-5 mode 0 with a 64-long last mode through einplan_run_json: the
+    per-rank blocks of every grid the planner picks go to the resident-factor
+    kernel (L = 64 or a 16-multiple slice of it) and the device reductions."""
+    e = "ijklm,ja,ka,la,ma->ia"
+    ext = dict(i=16, j=8, k=8, l=8, m=64, a=24)
+    s = eb.Session(e, ext)
+    path = f"/tmp/eb_out_rf_{P}.jsonl"
+    st, rep = s.run_json(P, 1024.0, seed=77, verify=False, dump_output=path)
+    assert st == 0, rep
+    ops = oracle.seeded_inputs(e, ext, 77)
+    check(np.loadtxt(path, skiprows=1), oracle.naive_evaluate(e, ext, ops))
+
+
 def _random_case(rng):
     """A random MTTKRP (any mode, order 3-5) or TTMc (order 3-4) einsum with
     small, often odd / ragged extents and a random processor count."""
