@@ -781,18 +781,21 @@ constexpr int kMaxCtas = 1024;
 __global__ void __launch_bounds__(kReduceGroups * 64)
     reduce_partials_kernel(const double* __restrict__ ws, double* __restrict__ out, int64_t M,
                             int R, int col0, int64_t ldo, int NP, int MT, int SPL,
-                            int64_t per_tile, int64_t items, int G, int segmax) {
+                            int64_t per_tile, int64_t items, int G, int segmax, int RPB) {
+  // block = RPB consecutive rows of one row tile (MT % RPB == 0): they share
+  // the CTA -> slot table; thread = (group, row, column), every thread busy
   __shared__ int64_t slot_base[kMaxCtas];
   __shared__ double part[kReduceGroups][64];
-  const int64_t m = blockIdx.x;
-  const int n = threadIdx.x % 64, grp = threadIdx.x / 64;
-  const int64_t t = m / MT;
+  const int64_t m0 = (int64_t)blockIdx.x * RPB;
+  const int n = threadIdx.x % NP, rr = (threadIdx.x / NP) % RPB, grp = threadIdx.x / (NP * RPB);
+  const int64_t m = m0 + rr;
+  const int64_t t = m0 / MT;
   const int64_t lo = t * per_tile, hi = lo + per_tile;
   const int64_t cmin = ((lo + 1) * G + items - 1) / items - 1;
   const int64_t cmax = (hi * G + items - 1) / items - 1;
   const int64_t cbeg = cmin < 0 ? 0 : cmin;
   const int nc = (int)((cmax < G - 1 ? cmax : G - 1) + 1 - cbeg);
-  for (int j = threadIdx.x; j < nc; j += kReduceGroups * 64) {
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) {
     const int64_t c = cbeg + j;
     const int64_t c0 = c * items / G, c1 = (c + 1) * items / G;
     slot_base[j] = (c1 <= lo || c0 >= hi || c1 <= c0) ? -1 : (c * segmax + (t - c0 / per_tile)) * SPL;
@@ -801,30 +804,28 @@ __global__ void __launch_bounds__(kReduceGroups * 64)
   const int total = nc * SPL;
   const int mr = (int)(m % MT);
   double acc = 0.0;
-  if (n < NP) {
-    constexpr int kBatch = 8;
-    for (int b = grp; b < total; b += kReduceGroups * kBatch) {
-      double v[kBatch];
+  constexpr int kBatch = 8;
+  for (int b = grp; b < total; b += kReduceGroups * kBatch) {
+    double v[kBatch];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        v[u] = 0.0;
-        const int e = b + u * kReduceGroups;
-        if (e < total) {
-          const int j = e / SPL, k = e - j * SPL;
-          const int64_t base = slot_base[j];
-          if (base >= 0) v[u] = ws[((base + k) * MT + mr) * NP + n];
-        }
+    for (int u = 0; u < kBatch; ++u) {
+      v[u] = 0.0;
+      const int e = b + u * kReduceGroups;
+      if (e < total) {
+        const int j = e / SPL, k = e - j * SPL;
+        const int64_t base = slot_base[j];
+        if (base >= 0) v[u] = ws[((base + k) * MT + mr) * NP + n];
       }
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) acc += v[u];
     }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) acc += v[u];
   }
-  part[grp][n] = acc;
+  part[grp][rr * NP + n] = acc;
   __syncthreads();
-  if (grp == 0 && n < NP && col0 + n < R) {
+  if (grp == 0 && m < M && col0 + n < R) {
     double x = 0.0;
 #pragma unroll
-    for (int g2 = 0; g2 < kReduceGroups; ++g2) x += part[g2][n];
+    for (int g2 = 0; g2 < kReduceGroups; ++g2) x += part[g2][rr * NP + n];
     out[m * ldo + col0 + n] = x;
   }
 }
@@ -833,8 +834,10 @@ void launch_reduce(const double* ws, double* out, int64_t M, int R, int col0, in
                    int MT, int SPL, int64_t per_tile, int64_t items, int G, int segmax,
                    cudaStream_t st) {
   if (G > kMaxCtas) throw InvalidError("eb_contract: too many CTAs for the partial reduction");
-  reduce_partials_kernel<<<(unsigned)M, kReduceGroups * 64, 0, st>>>(
-      ws, out, M, R, col0, ldo, NP, MT, SPL, per_tile, items, G, segmax);
+  int rpb = 1;  // rows per block: fill 64 columns' worth of threads per group
+  while (rpb * 2 * NP <= 64 && MT % (rpb * 2) == 0) rpb *= 2;
+  reduce_partials_kernel<<<(unsigned)((M + rpb - 1) / rpb), kReduceGroups * NP * rpb, 0, st>>>(
+      ws, out, M, R, col0, ldo, NP, MT, SPL, per_tile, items, G, segmax, rpb);
   EB_CUDA(cudaGetLastError());
   count_launch();
 }
