@@ -2,7 +2,8 @@
 or timed A/B variants with CUDA events.
 
 usage: python tools/prof_contract.py CFG [REPS] [ENV=VAL,... ...]
-  CFG in c1, c2m0, c2m1, c2m2, c2pair (eb_mttkrp2: modes 0+1 in one pass), c3.  With variant args, the variants are run
+  CFG in c1, c2m0, c2m1, c2m2, c2pair (eb_mttkrp2: modes 0+1 in one pass), c3,
+  p8m0/p8m1/p8m2 (C2's per-GPU 512^3 block at P = 8).  With variant args, the variants are run
   round-robin (3 rounds) and the best ms / TFLOP/s of each is printed.
 """
 import ctypes
@@ -47,6 +48,13 @@ if cfg.startswith("c2"):
          "c2m1": lambda: desc(C.EB_ROW, 1024, 1024, 1, 1024, 32, X, Cm, [A], [], out),
          "c2m2": lambda: desc(C.EB_COL, 1024, 1024, 1024, 0, 32, X, B, [A], [], out)}[cfg]()
     flops = 2.0 * 1024 ** 3 * 32
+elif cfg.startswith("p8"):  # C2's per-GPU block at P=8 (grid i2 j2 k2): 512^3, R = 32
+    X = r(512, 512, 512); A, B, Cm = r(512, 32), r(512, 32), r(512, 32)
+    out = torch.zeros(512, 32, dtype=torch.float64, device=dev)
+    d = {"p8m0": lambda: desc(C.EB_ROW, 1, 512, 512, 512, 32, X, Cm, [], [B], out),
+         "p8m1": lambda: desc(C.EB_ROW, 512, 512, 1, 512, 32, X, Cm, [A], [], out),
+         "p8m2": lambda: desc(C.EB_COL, 512, 512, 512, 0, 32, X, B, [A], [], out)}[cfg]()
+    flops = 2.0 * 512 ** 3 * 32
 elif cfg == "c1":
     X = r(512, 512, 512); B, Cm = r(512, 24), r(512, 24)
     out = torch.zeros(512, 24, dtype=torch.float64, device=dev)
