@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     const int64_t fe = nm > 0 ? prm.mid.ext[nm - 1] : 1;
     const double* fl = nm > 0 ? prm.mid.ptr[nm - 1] : nullptr;
     const int64_t fld = nm > 0 ? prm.mid.ld[nm - 1] : 0;
-    const bool fast = nm > 0 && fe % OS == 0;  // then Q % OS == 0: no partial groups
+    const bool fast = nm > 0 && fe % OS == 0 && prm.Q % OS == 0;  // whole groups, one prefix each
     int64_t mt = i0 / OG;
     int64_t p = (i0 % OG) / QG, q = ((i0 % OG) % QG) * OS;
     int64_t dq = 0, rest = 0;
