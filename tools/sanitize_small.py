@@ -1,5 +1,5 @@
 """Small end-to-end exercise of every kernel (for compute-sanitizer runs):
-fused MTTKRP ROW/COL (REDUCE, OS=1/2), TTM (BATCHED), generic steps, group
+fused MTTKRP ROW/COL (REDUCE, OS=1/2), the resident-factor MTTKRP, TTM (BATCHED), generic steps, group
 sums and redistribution boxes at P=1,2,4."""
 import sys
 sys.path.insert(0, "/root/repo")
@@ -12,6 +12,7 @@ cases = [
     ("ijk,ia,ka->ja", dict(i=130, j=132, k=18, a=8), (1, 2)),
     ("ijk,ia,ja->ka", dict(i=12, j=10, k=136, a=24), (1, 4)),
     ("ijklm,ja,ka,la,ma->ia", dict(i=8, j=4, k=4, l=4, m=6, a=6), (1, 2)),
+    ("ijklm,ja,ka,la,ma->ia", dict(i=8, j=4, k=4, l=8, m=16, a=6), (1, 2)),  # resident factor
     ("ijk,jb,kc->ibc", dict(i=8, j=8, k=8, b=3, c=3), (1, 2)),
     ("ij,jk,kl->il", dict(i=12, j=10, k=8, l=6), (1, 4)),
 ]
