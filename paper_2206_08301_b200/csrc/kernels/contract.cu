@@ -39,6 +39,7 @@
 
 #include "../host/status.hpp"
 #include "device_common.cuh"
+#include "pdl.cuh"
 #include "tma_host.hpp"
 #include "rf.hpp"
 #include "einplan_b200.h"
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  grid_dep_wait();  // launched with PDL: the previous kernel's writes are visible from here
 
   const int64_t per_tile_items = prm.O * prm.KC;
   const int64_t mtiles_all = prm.items / per_tile_items;
@@ -786,6 +788,7 @@ __global__ void __launch_bounds__(kReduceGroups * 64)
   // the CTA -> slot table; thread = (group, row, column), every thread busy
   __shared__ int64_t slot_base[kMaxCtas];
   __shared__ double part[kReduceGroups][64];
+  grid_dep_wait();
   const int64_t m0 = (int64_t)blockIdx.x * RPB;
   const int n = threadIdx.x % NP, rr = (threadIdx.x / NP) % RPB, grp = threadIdx.x / (NP * RPB);
   const int64_t m = m0 + rr;
@@ -836,9 +839,9 @@ void launch_reduce(const double* ws, double* out, int64_t M, int R, int col0, in
   if (G > kMaxCtas) throw InvalidError("eb_contract: too many CTAs for the partial reduction");
   int rpb = 1;  // rows per block: fill 64 columns' worth of threads per group
   while (rpb * 2 * NP <= 64 && MT % (rpb * 2) == 0) rpb *= 2;
-  reduce_partials_kernel<<<(unsigned)((M + rpb - 1) / rpb), kReduceGroups * NP * rpb, 0, st>>>(
-      ws, out, M, R, col0, ldo, NP, MT, SPL, per_tile, items, G, segmax, rpb);
-  EB_CUDA(cudaGetLastError());
+  launch_pdl(reduce_partials_kernel, dim3((unsigned)((M + rpb - 1) / rpb)),
+             dim3(kReduceGroups * NP * rpb), 0, st, ws, out, M, R, col0, ldo, NP, MT, SPL,
+             per_tile, items, G, segmax, rpb);
   count_launch();
 }
 
@@ -862,6 +865,7 @@ __global__ void reduce_two_kernel(const double* __restrict__ slots, double* __re
 // Uᵀ staging for the ROW variant (TMA needs k innermost): ut[n][l] = u[l][col0+n].
 __global__ void transpose_factor_kernel(const double* __restrict__ u, int64_t ldu, int64_t L,
                                         int cols, int col0, double* __restrict__ ut, int64_t ldt) {
+  grid_dep_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)cols * L) return;
   const int n = (int)(idx / L);
@@ -873,6 +877,7 @@ __global__ void transpose_factor_kernel(const double* __restrict__ u, int64_t ld
 // multiples of 16 B).
 __global__ void pitch_factor_kernel(const double* __restrict__ u, int64_t ldu, int64_t Q, int R,
                                     double* __restrict__ up, int64_t pitch) {
+  grid_dep_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= Q * pitch) return;
   const int64_t q = idx / pitch;
@@ -1005,8 +1010,7 @@ void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams
     attr = true;
   }
   main_kernel_begin(st);
-  kern<<<prm.G, (NWM * KS * OS + 1) * 32, T::kSmem, st>>>(xm, um, prm);
-  EB_CUDA(cudaGetLastError());
+  launch_pdl(kern, dim3(prm.G), dim3((NWM * KS * OS + 1) * 32), T::kSmem, st, xm, um, prm);
   main_kernel_end(st);
   count_launch();
 }
@@ -1088,9 +1092,8 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   CUtensorMap umap_col;
   if (p.col) {
     const int64_t n = d->Q * pitch;
-    pitch_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->Q, (int)d->R, ubuf,
-                                                                 pitch);
-    EB_CUDA(cudaGetLastError());
+    launch_pdl(pitch_factor_kernel, dim3((unsigned)cdiv(n, 256)), dim3(256), 0, st, d->U, ldu,
+               d->Q, (int)d->R, ubuf, pitch);
     count_launch();
     if (prm.fused_tma) {
       const uint64_t dims[3] = {16, (uint64_t)d->Q, (uint64_t)(pitch / 16)};
@@ -1140,9 +1143,8 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     if (!p.col) {
       const int64_t lp = (d->L + 1) / 2 * 2;
       const int64_t n = (int64_t)cols * d->L;
-      transpose_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->L, cols, col0,
-                                                                       ubuf, lp);
-      EB_CUDA(cudaGetLastError());
+      launch_pdl(transpose_factor_kernel, dim3((unsigned)cdiv(n, 256)), dim3(256), 0, st, d->U,
+                 ldu, d->L, cols, col0, ubuf, lp);
       count_launch();
       if (prm.fused_tma) {
         const uint64_t dims[3] = {16, (uint64_t)cols, (uint64_t)(d->L / 16)};

@@ -34,6 +34,7 @@
 #include "../host/status.hpp"
 #include "device_common.cuh"
 #include "einplan_b200.h"
+#include "pdl.cuh"
 #include "rf.hpp"
 #include "tma_host.hpp"
 
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  grid_dep_wait();  // launched with PDL
   const int64_t i0 = (int64_t)blockIdx.x * prm.items / prm.G;
   const int64_t i1 = (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
   if (i0 >= i1) return;
@@ -391,8 +393,7 @@ void rf_launch(const CUtensorMap& xm, const RfParams& prm, cudaStream_t st) {
     attr = true;
   }
   main_kernel_begin(st);
-  kern<<<prm.G, 9 * 32, smem, st>>>(xm, prm);
-  EB_CUDA(cudaGetLastError());
+  launch_pdl(kern, dim3(prm.G), dim3(9 * 32), smem, st, xm, prm);
   main_kernel_end(st);
   count_launch();
 }
