@@ -20,6 +20,7 @@
 #include <cstring>
 
 #include "../host/status.hpp"
+#include "pdl.cuh"
 #include "einplan_b200.h"
 
 namespace eb {
@@ -38,6 +39,7 @@ __global__ void __launch_bounds__(kThreads)
     hadamard_reduce_kernel(const double* __restrict__ T, const double* __restrict__ F,
                            double* __restrict__ out, int64_t I, int64_t J, int R, int axis) {
   __shared__ double part[kThreads];
+  grid_dep_wait();
   const int64_t row = blockIdx.x;
   const int groups = kThreads / R;
   const int r = threadIdx.x % R, grp = threadIdx.x / R;
@@ -74,6 +76,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     gram_partial_kernel(const double* __restrict__ F, int64_t n, int R, double* __restrict__ P) {
   __shared__ double tile[kGramRows][kMaxR + 1];
+  grid_dep_wait();
   const int64_t k0 = (int64_t)blockIdx.x * kGramRows;
   const int rows = (int)((n - k0) < kGramRows ? (n - k0) : kGramRows);
   for (int x = threadIdx.x; x < rows * R; x += blockDim.x) tile[x / R][x % R] = F[k0 * R + x];
@@ -89,6 +92,7 @@ __global__ void __launch_bounds__(kThreads)
 
 // G[x] = sum_b P[b][x] in ascending b (deterministic).
 __global__ void gram_sum_kernel(const double* __restrict__ P, int nb, int R, double* __restrict__ G) {
+  grid_dep_wait();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= R * R) return;
   double s = 0.0;
@@ -107,6 +111,7 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double colp[kMaxR], rowp[kMaxR];
   __shared__ double inv_s;
   constexpr int kPer = kMaxR * kMaxR / kThreads;  // entries per thread (R <= 64)
+  grid_dep_wait();
   int ii[kPer], jj[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
@@ -145,6 +150,7 @@ __global__ void __launch_bounds__(kThreads)
                          int R, double* __restrict__ Fout) {
   __shared__ double V[kMaxR * kMaxR];
   __shared__ double Ms[kThreads];
+  grid_dep_wait();
   const int rows = kThreads / R;
   const int64_t i0 = (int64_t)blockIdx.x * rows;
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) V[x] = Vinv[x];
@@ -244,25 +250,26 @@ void run_sweep(const double* X, int64_t I, int64_t J, int64_t K, int64_t R, doub
   const int Ri = (int)R;
   auto gram = [&](const double* F, int64_t n, double* G) {
     const int nb = (int)((n + kGramRows - 1) / kGramRows);
-    gram_partial_kernel<<<nb, kThreads, 0, st>>>(F, n, Ri, GP);
+    launch_pdl(gram_partial_kernel, dim3(nb), dim3(kThreads), 0, st, F, n, Ri, GP);
     EB_CUDA(cudaGetLastError());
-    gram_sum_kernel<<<(Ri * Ri + 255) / 256, 256, 0, st>>>(GP, nb, Ri, G);
+    launch_pdl(gram_sum_kernel, dim3((Ri * Ri + 255) / 256), dim3(256), 0, st, GP, nb, Ri, G);
     EB_CUDA(cudaGetLastError());
     count_launch();
     count_launch();
   };
   auto solve = [&](const double* Ga_, const double* Gb_, int64_t n, double* F) {
-    spd_inverse_kernel<<<1, kThreads, 0, st>>>(Ga_, Gb_, Ri, Vinv);
+    launch_pdl(spd_inverse_kernel, dim3(1), dim3(kThreads), 0, st, Ga_, Gb_, Ri, Vinv);
     EB_CUDA(cudaGetLastError());
     const int rows = kThreads / Ri;
-    apply_inverse_kernel<<<(unsigned)((n + rows - 1) / rows), kThreads, 0, st>>>(M, Vinv, n, Ri, F);
+    launch_pdl(apply_inverse_kernel, dim3((unsigned)((n + rows - 1) / rows)), dim3(kThreads), 0,
+               st, M, Vinv, n, Ri, F);
     EB_CUDA(cudaGetLastError());
     count_launch();
     count_launch();
   };
   auto hreduce = [&](const double* F, int axis) {
-    hadamard_reduce_kernel<<<(unsigned)(axis == 0 ? I : J), kThreads, 0, st>>>(T, F, M, I, J, Ri,
-                                                                              axis);
+    launch_pdl(hadamard_reduce_kernel, dim3((unsigned)(axis == 0 ? I : J)), dim3(kThreads), 0, st,
+               T, F, M, I, J, Ri, axis);
     EB_CUDA(cudaGetLastError());
     count_launch();
   };
