@@ -42,6 +42,7 @@
 
 #include "../host/status.hpp"
 #include "device_common.cuh"
+#include "pdl.cuh"
 #include "einplan_b200.h"
 #include "tma_host.hpp"
 
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  grid_dep_wait();  // launched with PDL
 
   if (warp == NW) {
     // ------------------------------------------------------------ producer
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     mbar_fence_init();
   }
   __syncthreads();
+  grid_dep_wait();  // launched with PDL
 
   if (warp == kWsS0 + kWsS1) {
     // ------------------------------------------------------------ producer
@@ -555,8 +558,7 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
     attr = true;
   }
   main_kernel_begin(st);
-  ttm2_kernel<NW, PIPE><<<prm.G, (NW + 1) * 32, Cfg<NW>::Smem, st>>>(xmap, prm);
-  EB_CUDA(cudaGetLastError());
+  launch_pdl(ttm2_kernel<NW, PIPE>, dim3(prm.G), dim3((NW + 1) * 32), Cfg<NW>::Smem, st, xmap, prm);
   main_kernel_end(st);
   count_launch();
 }
@@ -570,8 +572,8 @@ void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) 
     attr = true;
   }
   main_kernel_begin(st);
-  ttm2_ws_kernel<JP><<<prm.G, WsCfg<JP>::Warps * 32, WsCfg<JP>::Smem, st>>>(xmap, prm);
-  EB_CUDA(cudaGetLastError());
+  launch_pdl(ttm2_ws_kernel<JP>, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), WsCfg<JP>::Smem, st,
+             xmap, prm);
   main_kernel_end(st);
   count_launch();
 }
