@@ -285,9 +285,16 @@ __device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
 // then M += KRP[o] (.) T once per outer index — the Khatri-Rao product is a
 // per-column scale of T and is never formed.  One partial per k-split group.
 // BATCHED (TTM) requires KS == 1 and writes each (row tile, o) unit once.
+// WS: 12 warps instead of NCW + 1 = 9 — the third warpgroup (producer warp
+// NCW + three idle warps) hands registers to the two consumer warpgroups
+// (setmaxnreg 88 / 208 instead of a flat 168), which lets the
+// dimension-tree kernel (TWO) keep the 16-byte fragment loads and the lane-
+// per-column KRP path: 2 % faster pair; the single-output kernels gain
+// nothing from it (measured), so only TWO uses it.  The setmaxnreg calls sit
+// inside the role branches so ptxas budgets each region separately.
 template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
-          bool DIR = false>
-__global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
+          bool DIR = false, bool WS = false>
+__global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
   static_assert(KD % (16 * KS) == 0, "each k-split group owns whole 16-deep groups");
@@ -323,6 +330,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   }
   __syncthreads();
   grid_dep_wait();  // launched with PDL: the previous kernel's writes are visible from here
+  static_assert(!WS || NWM * KS * OS == 8, "WS: two consumer warpgroups");
 
   const int64_t per_tile_items = prm.O * prm.KC;
   const int64_t mtiles_all = prm.items / per_tile_items;
@@ -331,8 +339,12 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   const int64_t i1 = DIR ? ((int64_t)(blockIdx.x + 1) * mtiles_all / prm.G) * per_tile_items
                         : (int64_t)(blockIdx.x + 1) * prm.items / prm.G;
 
-  if (warp == NCW) {
+  if (warp >= NCW) {
     // ------------------------------------------------------------ producer
+    if constexpr (WS) {  // warpgroup 2: shrink, keep one warp
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+      if (warp != NCW) return;
+    }
     if (lane == 0) {
       tma_prefetch_desc(&xmap);
       tma_prefetch_desc(&umap);
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
     // what gates the ring (the general slot path below costs ~2.5k cycles
     // per order-5 stage).  The last factor's column block sits in shared
     // memory when it fits.
-    constexpr bool kLaneCol = NP <= 32 && !TWO;  // (TWO sits at the register cap)
+    constexpr bool kLaneCol = NP <= 32 && (!TWO || WS);  // (TWO at 168 registers: no room)
     const FacList& lastf = krp_last_list(prm, COL);
     const int64_t fe = has_krp ? lastf.ext[lastf.n - 1] : 1;
     const bool fast = kLaneCol && !BATCHED && has_krp && fe % OS == 0;
@@ -523,6 +535,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
   }
 
   // -------------------------------------------------------------- consumers
+  if constexpr (WS) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
   const int wm = warp % NWM, ks = (warp / NWM) % KS, os = warp / (NWM * KS);
   const int g = lane >> 2, l = lane & 3;
   double acc[MI][NT][2];                 // T: this outer index (or the TTM unit)
@@ -620,7 +633,7 @@ __global__ void __launch_bounds__((NWM * KS * OS + 1) * 32, 1)
       const uint8_t* xs = sbase + st * T::kStageBytes;
       const uint8_t* us = xs + T::kXBytes;
 #pragma unroll
-      if constexpr (!COL && !TWO) {  // (TWO sits at the register cap: 8-B loads)
+      if constexpr (!COL && (!TWO || WS)) {  // (TWO at 168 registers: 8-B loads)
 #pragma unroll
         for (int b16 = ks; b16 < KD / 16; b16 += KS)  // this warp's 16-deep k groups
 #pragma unroll
@@ -999,18 +1012,19 @@ Plan plan_of(const eb_contract_desc* d) {
 }
 
 template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
-          bool DIR = false>
+          bool DIR = false, bool WS = false>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
   using T = Tile<COL, NWM * WM, NT, KD, OS>;
-  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR, WS>;
   static bool attr = false;
   if (!attr) {
     EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
     attr = true;
   }
   main_kernel_begin(st);
-  launch_pdl(kern, dim3(prm.G), dim3((NWM * KS * OS + 1) * 32), T::kSmem, st, xm, um, prm);
+  launch_pdl(kern, dim3(prm.G), dim3(WS ? 384 : (NWM * KS * OS + 1) * 32), T::kSmem, st, xm, um,
+             prm);
   main_kernel_end(st);
   count_launch();
 }
@@ -1270,7 +1284,7 @@ void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, doub
   prm.ldo = d->R;
   switch (nt) {
 #define EB_TWO_CASE(N) \
-  case N: launch_t<false, false, 8, 16, 1, 32, 1, N, true>(xmap, umap, prm, st); break;
+  case N: launch_t<false, false, 8, 16, 1, 32, 1, N, true, false, true>(xmap, umap, prm, st); break;
     EB_TWO_CASE(1) EB_TWO_CASE(2) EB_TWO_CASE(3) EB_TWO_CASE(4)
     EB_TWO_CASE(5) EB_TWO_CASE(6) EB_TWO_CASE(7) EB_TWO_CASE(8)
 #undef EB_TWO_CASE
