@@ -330,6 +330,53 @@ def test_contract_order5_all_krp_rows(eb):
     check(got, want)
 
 
+def test_back_to_back_contractions_share_workspace(eb):
+    """Alternating contractions (general ROW, COL, resident-factor) reuse one
+    workspace with no host sync between them: every kernel of the chain is
+    launched with programmatic dependent launch, so this checks that none
+    touches global memory before its grid-dependency wait (a staging kernel
+    overwriting factors the previous contraction still reads would show)."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    rng = np.random.default_rng(5)
+    I, J, K, R = 160, 96, 64, 24
+    X = rng.uniform(-1, 1, (I, J, K))
+    gX = torch.from_numpy(X).cuda()
+    L_ = C.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    outs, wants = [], []
+    for it in range(12):
+        A, B, Cf = (rng.uniform(-1, 1, (n, R)) for n in (I, J, K))
+        gA, gB, gC = (torch.from_numpy(a).cuda() for a in (A, B, Cf))
+        out = torch.zeros(I if it % 3 != 2 else K, R, dtype=torch.float64, device="cuda")
+        d = C.ContractDesc()
+        if it % 3 == 0:    # mode 0, general ROW kernel (M = 160 >= 128)
+            d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_ROW, C.EB_REDUCE, 1, I, J, K, R
+            d.U, d.n_mid = gC.data_ptr(), 1
+            d.mid[0] = C.Factor(gB.data_ptr(), J, R)
+            want = np.einsum("ijk,jr,kr->ir", X, B, Cf)
+        elif it % 3 == 1:  # mode 0 on 64-row slab: resident-factor kernel (L = 64)
+            d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_ROW, C.EB_REDUCE, 1, 64, J, K, R
+            d.U, d.n_mid = gC.data_ptr(), 1
+            d.mid[0] = C.Factor(gB.data_ptr(), J, R)
+            want = np.zeros((I, R))
+            want[:64] = np.einsum("ijk,jr,kr->ir", X[:64], B, Cf)
+        else:              # mode 2, COL kernel
+            d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_COL, C.EB_REDUCE, I, K, J, 0, R
+            d.U, d.n_pre = gB.data_ptr(), 1
+            d.pre[0] = C.Factor(gA.data_ptr(), I, R)
+            want = np.einsum("ijk,ir,jr->kr", X, A, B)
+        d.X, d.ldu, d.out = gX.data_ptr(), R, out.data_ptr()
+        assert L_.eb_contract_workspace(ctypes.byref(d)) <= ws.numel()
+        C.check(L_.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), ws.numel(), st))
+        outs.append((out, gA, gB, gC))  # keep the factors alive until the sync
+        wants.append(want)
+    torch.cuda.synchronize()
+    for (out, *_), want in zip(outs, wants):
+        check(out.cpu().numpy(), want)
+
+
 RF_CASES = [  # (einsum, extents, P, M, Q, L, #pre, #mid): the resident-factor path
     ("ijklm,ja,ka,la,ma->ia", dict(i=40, j=6, k=7, l=5, m=64, a=24), 1, 40, 210, 64, 0, 3),
     ("ijkl,ja,ka,la->ia", dict(i=100, j=9, k=4, l=32, a=16), 1, 100, 36, 32, 0, 2),
