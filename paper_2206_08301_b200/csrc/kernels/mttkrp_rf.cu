@@ -9,19 +9,22 @@
 //
 // * every consumer lane holds its B fragments of U for the whole kernel, so
 //   the DMMA loop reads only X from shared memory (one 16-B load per two
-//   k-steps per m8 tile) — no U tile per stage, no B loads;
-// * a stage is one outer index o = (p, q): the 64 x L block X[p, 0:64, q, :]
-//   (one 5-D TMA box, SWIZZLE_128B), so an 8-KB-per-16-deep ring of up to 8
-//   stages keeps ~190 KB in flight per SM;
-// * T_o = X_o U accumulates in a fresh register tile per outer index; the
-//   Khatri-Rao row KRP[o] (computed per stage by the producer warp, one lane
-//   per column, incremental over the last factor's digit) scales it into the
-//   row tile's accumulator one stage later (M += KRP[o] (.) T_o as DFMAs on
-//   the same pipe, ~1.6 % of the DMMA work), so the fold never waits on the
-//   DMMA latency;
-// * CTAs take equal contiguous ranges of the (row tile, outer index) items and
-//   leave one partial per row tile they touch; eb_reduce_partials (contract.cu)
-//   sums them in CTA order — deterministic, no FP64 atomics.
+//   k-steps per m8 row fragment) — no U tile per stage, no B loads;
+// * a stage is one 5-D TMA box (SWIZZLE_128B) of RT rows x OS consecutive
+//   outer indices x L: 16 x 8 x 64 for C3, 64 KB, 4 KB contiguous per X row,
+//   three stages in flight;
+// * warp w owns one m8 row fragment and OS*RT/64 of the stage's outer indices;
+//   T_o = X_o U accumulates in a fresh register tile per outer index and is
+//   folded into the row tile's accumulator (M += KRP[o] (.) T_o, DFMA, ~1.6 %
+//   of the DMMA work) during the next outer index's first DMMAs, so the fold
+//   never waits on the DMMA latency;
+// * the producer warp issues the TMA box and writes the stage's KRP rows
+//   (lane = column; the OS outer indices of a stage share one prefix, so a
+//   value is one load and one multiply);
+// * CTAs take equal contiguous ranges of the (row tile, outer-index group)
+//   items and leave one partial per (row tile, warp group) they touch;
+//   reduce_partials_kernel (contract.cu) sums them in CTA order —
+//   deterministic, no FP64 atomics.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -58,7 +61,7 @@ struct RfParams {
   RfFacs pre, mid;
   const double* U;
   int64_t ldu;
-  double* part;  // [G][segmax][64][NP]
+  double* part;  // [G][segmax][SPL][RT][NP] partial slots
 };
 
 // KRP(list)[x, c], x decomposed row-major over the list's extents, skipping
@@ -75,8 +78,8 @@ __device__ double rf_krp(const RfFacs& f, int skip_last, int64_t x, int c) {
 
 // Stage = RT rows x OS consecutive outer indices x L: one TMA box
 // {16, RT, OS, KB, 1} -> smem [KB][OS][RT][16 doubles]; every X row
-// contributes one contiguous OS*L*8-byte run (long runs keep HBM efficient —
-// 64 rows x 512 B at a 128 MB stride streamed at 4.6 TB/s only).
+// contributes one contiguous OS*L*8-byte run (C3: 16 x 8 ran 1.63 ms,
+// 64 x 1 1.87, 32 x 4 1.96 — DESIGN.md §5).
 template <int RT, int OS, int KB>
 struct RfTile {
   static constexpr int kStageBytes = RT * OS * KB * 128;
@@ -111,18 +114,17 @@ __device__ __forceinline__ void rf_step(double (&t)[NF][2], const double (&tp)[N
                                         int lane) {
 #pragma unroll
   for (int nf = 0; nf < NF; ++nf) t[nf][0] = t[nf][1] = 0.0;
-
 #pragma unroll
   for (int kb = 0; kb < KB; ++kb) {
 #pragma unroll
-      for (int sp = 0; sp < 2; ++sp) {  // k = 16kb + 4l + 2sp + {0, 1}: chunk 2l + sp of the row
-        const double2 a =
-            *reinterpret_cast<const double2*>(xa + kb * KSTRIDE + (((2 * l + sp) ^ g) << 4));
+    for (int sp = 0; sp < 2; ++sp) {  // k = 16kb + 4l + 2sp + {0, 1}: chunk 2l + sp of the row
+      const double2 a =
+          *reinterpret_cast<const double2*>(xa + kb * KSTRIDE + (((2 * l + sp) ^ g) << 4));
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) dmma884(t[nf][0], t[nf][1], a.x, e[kb][2 * sp][nf]);
+      for (int nf = 0; nf < NF; ++nf) dmma884(t[nf][0], t[nf][1], a.x, e[kb][2 * sp][nf]);
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) dmma884(t[nf][0], t[nf][1], a.y, e[kb][2 * sp + 1][nf]);
-      }
+      for (int nf = 0; nf < NF; ++nf) dmma884(t[nf][0], t[nf][1], a.y, e[kb][2 * sp + 1][nf]);
+    }
     if (kb == 0 && pend) {
       rf_fold<NF>(acc, tp, sprev, l);
       if (release) {
