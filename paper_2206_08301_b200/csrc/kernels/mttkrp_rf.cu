@@ -11,8 +11,7 @@
 //   the DMMA loop reads only X from shared memory (one 16-B load per two
 //   k-steps per m8 row fragment) — no U tile per stage, no B loads;
 // * a stage is one 5-D TMA box (SWIZZLE_128B) of RT rows x OS consecutive
-//   outer indices x L: 16 x 8 x 64 for C3, 64 KB, 4 KB contiguous per X row,
-//   three stages in flight;
+//   outer indices x L: 16 x 8 x 64 for C3, 64 KB, three stages in flight;
 // * warp w owns one m8 row fragment and OS*RT/64 of the stage's outer indices;
 //   T_o = X_o U accumulates in a fresh register tile per outer index and is
 //   folded into the row tile's accumulator (M += KRP[o] (.) T_o, DFMA, ~1.6 %
@@ -81,9 +80,9 @@ __device__ double rf_krp(const RfFacs& f, int skip_last, int64_t x, int c) {
 }
 
 // Stage = RT rows x OS consecutive outer indices x L: one TMA box
-// {16, RT, OS, KB, 1} -> smem [KB][OS][RT][16 doubles]; every X row
-// contributes one contiguous OS*L*8-byte run (C3: 16 x 8 ran 1.63 ms,
-// 64 x 1 1.87, 32 x 4 1.96 — DESIGN.md §5).
+// {16, RT, OS, KB, 1} -> smem [KB][OS][RT][16 doubles] (C3: 16 x 8 ran
+// 1.63 ms, 64 x 1 1.87, 32 x 4 1.96 — per-stage overhead, not run length:
+// DESIGN.md §5).
 template <int RT, int OS, int KB>
 struct RfTile {
   static constexpr int kStageBytes = RT * OS * KB * 128;
@@ -445,7 +444,7 @@ bool rf_plan(const eb_contract_desc* d, RfPlan& p) {
   if (d->Q > INT32_MAX || d->P > INT32_MAX) return false;
   p.kb = (int)(d->L / 16);
   p.nf = (int)cdiv(d->R, 8);
-  // 16 rows x 8 outer indices per stage (4 KB runs per X row at L = 64);
+  // 16 rows x 8 outer indices per stage (two outer indices per warp per stage);
   // one outer index of 64 rows when the mid extent is short
   p.rt = 16;
   p.os = 8;
