@@ -10,7 +10,7 @@ NCU="ncu --clock-control none"
 $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_bench.log 2>&1
 # 2) full captures of the dominant kernel per configuration
-for c in c2m0 c2m2 c2pair c1; do
+for c in c2m0 c2m1 c2m2 c2pair c1; do
   timeout 600 $NCU --set full --import-source on -k regex:contract_kernel -c 1 -o $O/ncu_$c \
     python tools/prof_contract.py $c 2 > $O/ncu_$c.log 2>&1
 done
