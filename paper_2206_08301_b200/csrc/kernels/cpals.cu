@@ -101,46 +101,48 @@ __global__ void gram_sum_kernel(const double* __restrict__ P, int nb, int R, dou
 }
 
 // Vinv = (Ga (.) Gb)^-1 by Gauss-Jordan elimination without pivoting (V is
-// symmetric positive definite: every pivot is positive), one block, V in
-// shared memory: step p updates all R x R entries in parallel from the old
-// pivot row and column (two barriers per step, R steps).
-__global__ void __launch_bounds__(kThreads)
+// symmetric positive definite: every pivot is positive), one block of
+// kInvThreads, V double-buffered in shared memory: step p computes every
+// entry of the next buffer from the current one (pivot row, pivot column,
+// the entry itself; each thread forms 1/pivot itself) — one barrier per
+// step, R steps.
+constexpr int kInvThreads = 1024;
+__global__ void __launch_bounds__(kInvThreads)
     spd_inverse_kernel(const double* __restrict__ Ga, const double* __restrict__ Gb, int R,
                        double* __restrict__ Vinv) {
-  __shared__ double V[kMaxR][kMaxR + 1];
-  __shared__ double colp[kMaxR], rowp[kMaxR];
-  __shared__ double inv_s;
-  constexpr int kPer = kMaxR * kMaxR / kThreads;  // entries per thread (R <= 64)
+  extern __shared__ double vbuf[];  // 2 x [R][R + 1]
+  constexpr int kPer = kMaxR * kMaxR / kInvThreads;  // entries per thread (R <= 64)
+  const int ld = R + 1;
+  double* cur = vbuf;
+  double* nxt = vbuf + R * ld;
   grid_dep_wait();
   int ii[kPer], jj[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
-    const int x = threadIdx.x + u * kThreads;
+    const int x = threadIdx.x + u * kInvThreads;
     ii[u] = x < R * R ? x / R : -1;
     jj[u] = x < R * R ? x % R : 0;
-    if (ii[u] >= 0) V[ii[u]][jj[u]] = Ga[x] * Gb[x];
+    if (ii[u] >= 0) cur[ii[u] * ld + jj[u]] = Ga[x] * Gb[x];
   }
   __syncthreads();
   for (int p = 0; p < R; ++p) {
-    if (threadIdx.x < R) {
-      colp[threadIdx.x] = V[threadIdx.x][p];
-      rowp[threadIdx.x] = V[p][threadIdx.x];
-      if (threadIdx.x == 0) inv_s = 1.0 / V[p][p];
-    }
-    __syncthreads();
-    const double inv = inv_s;
+    const double inv = 1.0 / cur[p * ld + p];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int i = ii[u], j = jj[u];
       if (i < 0) continue;
-      const double f = colp[i], a = rowp[j];
-      V[i][j] = i == p ? (j == p ? inv : a * inv) : (j == p ? -f * inv : V[i][j] - f * a * inv);
+      const double f = cur[i * ld + p], a = cur[p * ld + j];
+      nxt[i * ld + j] =
+          i == p ? (j == p ? inv : a * inv) : (j == p ? -f * inv : cur[i * ld + j] - f * a * inv);
     }
     __syncthreads();
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
   }
 #pragma unroll
   for (int u = 0; u < kPer; ++u)
-    if (ii[u] >= 0) Vinv[ii[u] * R + jj[u]] = V[ii[u]][jj[u]];
+    if (ii[u] >= 0) Vinv[ii[u] * R + jj[u]] = cur[ii[u] * ld + jj[u]];
 }
 
 // Fout[i][s] = sum_r M[i][r] Vinv[r][s]: thread per output element, Vinv and
@@ -248,6 +250,10 @@ void run_sweep(const double* X, int64_t I, int64_t J, int64_t K, int64_t R, doub
   double* GP = reinterpret_cast<double*>(w + Ly.t + Ly.m + Ly.g);
   void* cw = w + Ly.t + Ly.m + Ly.g + Ly.gp;
   const int Ri = (int)R;
+  const size_t inv_smem = (size_t)2 * Ri * (Ri + 1) * sizeof(double);
+  if (inv_smem > 48 * 1024)
+    EB_CUDA(cudaFuncSetAttribute(spd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)inv_smem));
   auto gram = [&](const double* F, int64_t n, double* G) {
     const int nb = (int)((n + kGramRows - 1) / kGramRows);
     launch_pdl(gram_partial_kernel, dim3(nb), dim3(kThreads), 0, st, F, n, Ri, GP);
@@ -258,7 +264,7 @@ void run_sweep(const double* X, int64_t I, int64_t J, int64_t K, int64_t R, doub
     count_launch();
   };
   auto solve = [&](const double* Ga_, const double* Gb_, int64_t n, double* F) {
-    launch_pdl(spd_inverse_kernel, dim3(1), dim3(kThreads), 0, st, Ga_, Gb_, Ri, Vinv);
+    launch_pdl(spd_inverse_kernel, dim3(1), dim3(kInvThreads), inv_smem, st, Ga_, Gb_, Ri, Vinv);
     EB_CUDA(cudaGetLastError());
     const int rows = kThreads / Ri;
     launch_pdl(apply_inverse_kernel, dim3((unsigned)((n + rows - 1) / rows)), dim3(kThreads), 0,
