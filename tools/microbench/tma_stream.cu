@@ -2,7 +2,8 @@
 // warp per SM stream an 8.6 GB FP64 tensor through a 6 x 32 KB shared-memory
 // ring, as a function of the box shape (the contiguous run per X row)?
 // X is viewed as [i=64][j=64][k=64][lm=4096] (the C5 / C3 operand).  Each CTA
-// streams a contiguous range of boxes; the consumer warp only waits on the
+// streams a contiguous range of boxes (or, order 1, the ttm2 round-robin item
+// schedule); the consumer warp only waits on the
 // full barrier and releases the stage, so the time is the data path alone.
 // Output: one JSON object per pattern.
 //
@@ -30,7 +31,12 @@ constexpr int kStageBytes = 32 * 1024;
 struct Pattern {
   const char* name;
   uint32_t box[4];  // {lm, k, j, i}
+  int order;        // 0: contiguous ranges per CTA, 1: ttm2 round-robin items
 };
+
+__device__ __forceinline__ int64_t ni_of(int64_t nbox, int tl, int tk, int tj) {
+  return nbox / ((int64_t)tl * tk * tj);
+}
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -38,7 +44,7 @@ __device__ __forceinline__ uint32_t saddr(const void* p) {
 
 __global__ void __launch_bounds__(64, 1)
     stream_kernel(const __grid_constant__ CUtensorMap map, int64_t nbox, int nlm, int nk, int nj,
-                  int b0, int b1, int b2) {
+                  int b0, int b1, int b2, int order) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   const uint32_t base = (saddr(smem) + 1023u) & ~1023u;
@@ -60,16 +66,31 @@ __global__ void __launch_bounds__(64, 1)
       asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                    : "=r"(ok) : "r"(bar), "r"(par) : "memory");
   };
+  // order 0: contiguous box ranges per CTA (lm tile fastest, then k, j, i);
+  // order 1: the ttm2 schedule — items (i, lm tile) dealt round-robin to the
+  // CTAs, each item streamed as its k chunks (tj == 1: the box spans all j)
+  const int64_t nitems = (int64_t)ni_of(nbox, tl, tk, tj) * tl;
+  const int64_t mine = order == 0 ? (i1 - i0)
+                                  : ((nitems - blockIdx.x + gridDim.x - 1) / gridDim.x) * tk;
   if (threadIdx.x == 0) {
     uint32_t it = 0;
-    for (int64_t b = i0; b < i1; ++b, ++it) {
+    for (int64_t t = 0; t < mine; ++t, ++it) {
       const int st = it % kStages;
       if (it >= (uint32_t)kStages) wait(saddr(&empty[st]), ((it / kStages) - 1) & 1);
-      int64_t x = b;
-      const int c0 = (int)(x % tl) * b0; x /= tl;
-      const int c1 = (int)(x % tk) * b1; x /= tk;
-      const int c2 = (int)(x % tj) * b2; x /= tj;
-      const int c3 = (int)x;
+      int c0, c1, c2, c3;
+      if (order == 0) {
+        int64_t x = i0 + t;
+        c0 = (int)(x % tl) * b0; x /= tl;
+        c1 = (int)(x % tk) * b1; x /= tk;
+        c2 = (int)(x % tj) * b2; x /= tj;
+        c3 = (int)x;
+      } else {
+        const int64_t item = blockIdx.x + (t / tk) * gridDim.x;
+        c0 = (int)(item % tl) * b0;
+        c1 = (int)(t % tk) * b1;
+        c2 = 0;
+        c3 = (int)(item / tl);
+      }
       const uint32_t fb = saddr(&full[st]);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(kStageBytes) : "memory");
       asm volatile(
@@ -80,7 +101,7 @@ __global__ void __launch_bounds__(64, 1)
     }
   } else if (threadIdx.x == 32) {
     uint32_t it = 0;
-    for (int64_t b = i0; b < i1; ++b, ++it) {
+    for (int64_t t = 0; t < mine; ++t, ++it) {
       const int st = it % kStages;
       wait(saddr(&full[st]), (it / kStages) & 1);
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&empty[st])) : "memory");
@@ -106,11 +127,12 @@ int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const Pattern pats[] = {
-      {"lm16_k4_j64 (ttm2 term 0: 128 B runs)", {16, 4, 64, 1}},
-      {"lm32_k2_j64 (256 B runs)", {32, 2, 64, 1}},
-      {"lm64_k1_j64 (512 B runs)", {64, 1, 64, 1}},
-      {"lm128_k1_j32 (1 KB runs)", {128, 1, 32, 1}},
-      {"lm256_k1_j16 (2 KB runs)", {256, 1, 16, 1}},
+      {"lm16_k4_j64 (ttm2 term 0: 128 B runs)", {16, 4, 64, 1}, 0},
+      {"lm16_k4_j64, ttm2 round-robin item order", {16, 4, 64, 1}, 1},
+      {"lm32_k2_j64 (256 B runs)", {32, 2, 64, 1}, 0},
+      {"lm64_k1_j64 (512 B runs)", {64, 1, 64, 1}, 0},
+      {"lm128_k1_j32 (1 KB runs)", {128, 1, 32, 1}, 0},
+      {"lm256_k1_j16 (2 KB runs)", {256, 1, 16, 1}, 0},
   };
   CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kStages * kStageBytes + 1024));
@@ -138,7 +160,7 @@ int main() {
     for (int rep = 0; rep < 5; ++rep) {
       CK(cudaEventRecord(a));
       stream_kernel<<<sms, 64, kStages * kStageBytes + 1024>>>(m, nbox, nlm, nk, nj, pt.box[0],
-                                                               pt.box[1], pt.box[2]);
+                                                               pt.box[1], pt.box[2], pt.order);
       CK(cudaEventRecord(z));
       CK(cudaEventSynchronize(z));
       float ms = 0;
