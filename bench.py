@@ -599,7 +599,8 @@ def main():
         "config": {"workload": label, "procs": P, "fast_mem": 1024, "grids": grids,
                    "transport": "nccl" if use_nccl else "virtual",
                    "tree_flops_per_step": flops_tree,
-                   "l2": "inputs larger than L2 (X is 8.6 GB vs 126 MB L2), no flush needed"},
+                   "l2": "inputs larger than L2 (X is %.2f GB per GPU vs 126 MB L2), no flush "
+                         "needed" % (_x_bytes(modes[:1], P) / 1e9)},
         "roofline": roof,
         "e2e": e2e,
         **({"sweep_dimtree": alt} if alt else {}),
