@@ -330,6 +330,24 @@ def test_contract_order5_all_krp_rows(eb):
     check(got, want)
 
 
+@pytest.mark.parametrize("cfg", ["64x1", "32x2", "32x4", "16x4", "16x8", "8x8", "8x16"])
+def test_resident_factor_measurement_tilings(eb, cfg, monkeypatch):
+    """Every tiling the EB_RF_CFG measurement knob can select (the C3 term
+    shape, L = 64, R = 24) gives the oracle's result."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    monkeypatch.setenv("EB_RF_CFG", cfg)
+    e = "ijklm,ja,ka,la,ma->ia"
+    ext = dict(i=64, j=4, k=4, l=8, m=64, a=24)
+    ops = oracle.seeded_inputs(e, ext, 21)
+    want = oracle.naive_evaluate(e, ext, ops)
+    g = [torch.from_numpy(o).cuda() for o in ops]
+    out = torch.zeros(want.shape, dtype=torch.float64, device="cuda")
+    got = _contract(eb, C.EB_ROW, C.EB_REDUCE, 1, 64, 4 * 4 * 8, 64, 24, g[0], g[4], [], g[1:4],
+                    out)
+    check(got, want)
+
+
 def test_back_to_back_contractions_share_workspace(eb):
     """Alternating contractions (general ROW, COL, resident-factor) reuse one
     workspace with no host sync between them: every kernel of the chain is
