@@ -67,9 +67,12 @@ SHAPES3 = [(40, 36, 50, 24), (130, 20, 34, 32), (64, 64, 64, 64), (20, 9, 18, 70
 
 @pytest.mark.parametrize("I,J,K,R", SHAPES3)
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_contract_mttkrp_order3(eb, I, J, K, R, mode):
+@pytest.mark.parametrize("fused_tma", [True, False])
+def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, monkeypatch):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
+    if not fused_tma:  # one TMA box per 16-wide block instead of one per operand
+        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
     ext = dict(i=I, j=J, k=K, a=R)
     e = ["ijk,ja,ka->ia", "ijk,ia,ka->ja", "ijk,ia,ja->ka"][mode]
     ops = oracle.seeded_inputs(e, ext, 17 + mode)
@@ -110,11 +113,18 @@ TTM2_SHAPES = [(2, 64, 64, 64, 16, 16), (3, 40, 7, 50, 16, 16), (1, 64, 9, 18, 5
 
 
 @pytest.mark.parametrize("P,Q1,Q2,M,N1,N2", TTM2_SHAPES)
-def test_ttm2_pair(eb, P, Q1, Q2, M, N1, N2):
+@pytest.mark.parametrize("knob", ["", "EB_TTM2_WARPS=w1", "EB_TTM2_WARPS=w2", "EB_TTM2_WARPS=8",
+                                  "EB_TTM2_WARPS=16", "EB_TTM2_WARPS=8,EB_TTM2_PIPE=1"])
+def test_ttm2_pair(eb, P, Q1, Q2, M, N1, N2, knob, monkeypatch):
     """eb_ttm2 = the two chained TTM steps pjkm,jb->pkmb ; pkmb,kc->pmbc of one
-    term (TTMc-O5), ragged in every extent, against the oracle's n-ary loop."""
+    term (TTMc-O5), ragged in every extent, against the oracle's n-ary loop —
+    the shipped warp-specialised kernels (JP = 1 / 2) and the measured
+    alternatives the EB_TTM2_* knobs select."""
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
+    for kv in filter(None, knob.split(",")):
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     e = "pjkm,jb,kc->pmbc"
     ext = dict(p=P, j=Q1, k=Q2, m=M, b=N1, c=N2)
     ops = oracle.seeded_inputs(e, ext, 23)
@@ -405,11 +415,12 @@ RF_CASES = [  # (einsum, extents, P, M, Q, L, #pre, #mid): the resident-factor p
 
 
 @pytest.mark.parametrize("case", range(len(RF_CASES)))
-@pytest.mark.parametrize("knob", ["", "EB_RF_MI=2", "EB_NO_RF=1"])
+@pytest.mark.parametrize("knob", ["", "EB_RF_CFG=64x1", "EB_NO_RF=1"])
 def test_contract_resident_factor_path(eb, case, knob, monkeypatch):
     """Short contracted mode (L <= 64, L % 16 == 0), R <= 24, M < 128: the
-    resident-factor kernel (mttkrp_rf.cu; 8 x 8-row or 4 x 16-row consumer
-    warps) and, with EB_NO_RF, the general kernel — both against the oracle."""
+    resident-factor kernel (mttkrp_rf.cu; the paired 16 x 8 tiling, or the
+    64 x 1 one) and, with EB_NO_RF, the general kernel — all against the
+    oracle."""
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
     e, ext, P, M, Q, L, npre, nmid = RF_CASES[case]
