@@ -94,9 +94,12 @@ def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, monkeypatch):
 
 @pytest.mark.parametrize("I,J,K,B", [(5, 40, 34, 64), (3, 70, 130, 16), (4, 33, 64, 24),
                                      (2, 9, 2, 100), (1, 256, 258, 8)])
-def test_contract_ttm(eb, I, J, K, B):
+@pytest.mark.parametrize("fused_tma", [True, False])
+def test_contract_ttm(eb, I, J, K, B, fused_tma, monkeypatch):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
+    if not fused_tma:
+        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
     ext = dict(i=I, j=J, k=K, b=B)
     e = "ijk,jb->ikb"
     X, U = oracle.seeded_inputs(e, ext, 13)
@@ -189,10 +192,13 @@ MTTKRP2_SHAPES = [(130, 20, 34, 32), (256, 64, 64, 24), (128, 9, 2, 8), (300, 40
 
 
 @pytest.mark.parametrize("I,J,K,R", MTTKRP2_SHAPES)
-def test_mttkrp2_dimension_tree_pair(eb, I, J, K, R):
+@pytest.mark.parametrize("fused_tma", [True, False])
+def test_mttkrp2_dimension_tree_pair(eb, I, J, K, R, fused_tma, monkeypatch):
     """eb_mttkrp2: one pass over X gives the mode-0 and the mode-1 MTTKRP
     (T = X x_k C folded with B and with A), each equal to the oracle's own
     naive_evaluate of that mode's einsum."""
+    if not fused_tma:
+        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
     ext = dict(i=I, j=J, k=K, a=R)
