@@ -364,6 +364,36 @@ def test_resident_factor_measurement_tilings(eb, cfg, monkeypatch):
     check(got, want)
 
 
+@pytest.mark.parametrize("M,L", [(64, 64), (40, 32), (160, 64)])  # RF (x2) and general kernel
+def test_contract_padded_factor_rows(eb, M, L):
+    """Factors with a row pitch wider than R (ld = R + 5): the KRP loads, the
+    resident B fragments and the staged U tiles all honour ld."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    rng = np.random.default_rng(M + L)
+    J, K, R, pad = 6, 7, 20, 5
+    X = rng.uniform(-1, 1, (M, J, K, L))
+    F = [rng.uniform(-1, 1, (n, R + pad)) for n in (J, K, L)]
+    want = np.einsum("ijkl,ja,ka,la->ia", X, *(f[:, :R] for f in F))
+    gX = torch.from_numpy(X).cuda()
+    gF = [torch.from_numpy(f).cuda() for f in F]
+    out = torch.zeros(M, R, dtype=torch.float64, device="cuda")
+    d = C.ContractDesc()
+    d.variant, d.mode, d.P, d.M, d.Q, d.L, d.R = C.EB_ROW, C.EB_REDUCE, 1, M, J * K, L, R
+    d.X, d.U, d.ldu = gX.data_ptr(), gF[2].data_ptr(), R + pad
+    d.n_mid = 2
+    d.mid[0] = C.Factor(gF[0].data_ptr(), J, R + pad)
+    d.mid[1] = C.Factor(gF[1].data_ptr(), K, R + pad)
+    d.out = out.data_ptr()
+    L_ = C.lib()
+    wb = L_.eb_contract_workspace(ctypes.byref(d))
+    ws = torch.empty(max(wb, 8), dtype=torch.uint8, device="cuda")
+    C.check(L_.eb_contract(ctypes.byref(d), ctypes.c_void_p(ws.data_ptr()), wb,
+                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), want)
+
+
 def test_back_to_back_contractions_share_workspace(eb):
     """Alternating contractions (general ROW, COL, resident-factor) reuse one
     workspace with no host sync between them: every kernel of the chain is
