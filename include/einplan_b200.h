@@ -134,8 +134,16 @@ int eb_step_generic(const char* lhs_indices, const char* rhs_indices,
  * every member (executor.cpp:80-108). */
 int eb_group_sum(double* const* members, int n_members, int64_t n, void* stream);
 
+/* The same ascending-rank sum written to `dst` only (members are read, not
+ * written): the peer-memory allreduce, where members are the group's blocks
+ * in the peers' exchange heaps (executor.cpp:91-98). */
+int eb_group_sum_into(const double* const* members, int n_members, int64_t n, double* dst,
+                      void* stream);
+
 /* Strided box copy of one redistribution message between dense row-major
- * device blocks (redistribute.cpp:152-183). */
+ * device blocks (redistribute.cpp:152-183); src may be a peer-mapped pointer
+ * (the peer transport's pull).  Adjacent dims the box spans contiguously in
+ * both blocks are merged; rows move as 16-byte vectors when aligned. */
 int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst,
                 const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
                 const int64_t* ox_lo, void* stream);
@@ -155,13 +163,28 @@ void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip);
  * to the box's last element; memory O(box)) */
 int eb_random_fill_block(double* out, uint64_t seed, int nd, const int64_t* gshape,
                          const int64_t* base, const int64_t* shape);
+/* a stateful stream: consecutive eb_rng_fill calls continue where the last
+ * one stopped (e.g. the 64-row i-slabs of C5's global X one after another,
+ * one pass over the stream instead of one per slab) */
+typedef struct eb_rng eb_rng;
+int eb_rng_create(uint64_t seed, int64_t skip, eb_rng** out);
+void eb_rng_fill(eb_rng* g, double* out, int64_t n);
+void eb_rng_destroy(eb_rng* g);
 
 void eb_free(void* p);
+/* bytes in use in the current device's stream-ordered pool (where executors
+ * allocate their per-run blocks): flat across repeated runs */
+int eb_mem_in_use(int64_t* bytes);
 
 /* Host-only planning: plan_report(make_pipeline(...)) as einplan/v1 JSON
  * (schedule.cpp:72-80, report.cpp:194-199).  No device needed. */
 int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fast_mem,
                  int include_messages, char** json_out);
+
+/* Path options (read once from EB_* environment variables at load; this
+ * call changes them between runs): "no_fused_tma" 0/1, "no_rf" 0/1,
+ * "rf_cfg" "RTxOS"|"auto", "ttm2_variant" 0/1/2, "fuse_ttm2" 0/1. */
+int eb_set_option(const char* name, const char* value);
 
 /* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------
  * rank < 0: all `procs` ranks are virtual and resident on the current device
@@ -174,6 +197,15 @@ typedef struct eb_exec eb_exec;
 int eb_nccl_unique_id(void* out128);
 int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double fast_mem,
                    int64_t rank, const void* nccl_id, void* stream, eb_exec** out);
+/* rank `rank` of `procs` processes on one node exchanging over peer memory
+ * (CUDA IPC: the group's exchange heaps mapped by every rank; host barrier
+ * in the POSIX shared-memory segment `group`, e.g. "/eb_job42", the same
+ * string on every rank).  Works with one GPU per process (NVLink loads) and
+ * with several processes on one GPU (the multi-rank tests).  No kernel waits
+ * on another rank: each collective synchronises its stream, then meets the
+ * peers on the host.  Every rank must call eb_exec_run / eb_exec_gather. */
+int eb_exec_create_peer(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                        int64_t rank, const char* group, void* stream, eb_exec** out);
 /* a second executor over the same ranks and the same communicator as `peer`
  * (an ncclUniqueId initialises exactly one communicator): e.g. the three
  * MTTKRP modes of a sweep on one process group */
@@ -188,6 +220,11 @@ int eb_exec_stage(eb_exec* h, const double* const* host_inputs);
  * (row-major) — no process needs the global tensor */
 int eb_exec_block(eb_exec* h, int k, int64_t* base, int64_t* shape, int* nd);
 int eb_exec_stage_block(eb_exec* h, int k, const double* host_block);
+/* virtual ranks without the global tensor: operand k from a host buffer
+ * holding its global sub-box [base, base + shape) (row-major, nd dims); the
+ * owned ranks' blocks inside it are staged, *staged = how many */
+int eb_exec_stage_region(eb_exec* h, int k, const int64_t* base, const int64_t* shape, int nd,
+                         const double* host_region, int* staged);
 /* alias operand k_dst of `dst` to the staged device blocks of operand k_src of
  * `src` (same shape and placement on every owned rank, checked); `dst` then
  * stages NULL for it (e.g. one X shared by the three modes of a CP-ALS sweep) */
@@ -209,7 +246,8 @@ int eb_exec_join(eb_exec* h);
  * when the pair ran fused, 0 when it did not qualify and both executors were
  * run separately (same results). */
 int eb_exec_run_pair(eb_exec* mode0, eb_exec* mode1, int* fused);
-/* gather canonical output blocks to host (virtual mode, or rank 0) */
+/* gather canonical output blocks to host (virtual mode, or rank 0; other
+ * ranks pass NULL — collective for the peer transport) */
 int eb_exec_gather(eb_exec* h, double* host_out);
 int64_t eb_exec_output_elems(eb_exec* h);
 /* out8 = {allreduce_volume, redistribute_volume, max_rank_sent,

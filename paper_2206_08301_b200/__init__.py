@@ -9,7 +9,10 @@ that interface for Python callers:
 * :func:`bench_json` — ``einplan_bench_json`` (capi.cpp:228-254);
 * :class:`Executor` — the rank-local GPU executor (``eb_exec_*``): stage
   inputs once, run the schedule repeatedly with data resident in HBM, gather;
-  one process per GPU over NCCL when ``rank >= 0``;
+  one process per GPU over NCCL when ``rank >= 0``, or over peer memory
+  (CUDA IPC, ``transport="peer"``);
+* :func:`set_option` — the path options (``eb_set_option``);
+* :class:`RandomStream` — the reference input stream, consumed in order;
 * :func:`plan_json`, :func:`random_tensor` — host-only helpers.
 
 Compute happens only in ``lib/libeinplan_b200.so`` (sm_100a kernels).  There
@@ -25,8 +28,8 @@ import numpy as np
 from . import _capi
 from ._capi import EinplanError
 
-__all__ = ["Session", "Executor", "EinplanError", "bench_json", "plan_json", "random_tensor",
-           "version", "dims_string"]
+__all__ = ["Session", "Executor", "EinplanError", "RandomStream", "bench_json", "plan_json",
+           "random_tensor", "set_option", "version", "dims_string"]
 
 
 def version() -> str:
@@ -108,6 +111,53 @@ def cp3_als_sweep(X, A, B, C, stream=None, workspace=None):
     return workspace
 
 
+def set_option(name: str, value) -> None:
+    """Path options of the kernel layer (eb_set_option): "no_fused_tma",
+    "no_rf", "rf_cfg" ("RTxOS" / "auto"), "ttm2_variant" (0/1/2), "fuse_ttm2".
+    Read once from the EB_* environment at load; change them between runs."""
+    _capi.check(_capi.lib().eb_set_option(name.encode(), str(value).encode()))
+
+
+class RandomStream:
+    """random_tensor's mt19937_64 stream (tensor.cpp:55-63) consumed in order:
+    successive :meth:`fill` calls continue where the last one stopped."""
+
+    def __init__(self, seed: int, skip: int = 0):
+        self._h = ctypes.c_void_p()
+        _capi.check(_capi.lib().eb_rng_create(seed, skip, ctypes.byref(self._h)))
+
+    def fill(self, out: np.ndarray) -> np.ndarray:
+        if out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("RandomStream.fill: out must be a contiguous float64 array")
+        _capi.lib().eb_rng_fill(self._h, out.ctypes.data_as(_capi._dp), out.size)
+        return out
+
+    def close(self):
+        if self._h:
+            _capi.lib().eb_rng_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mem_in_use() -> int:
+    """Bytes in use in the current device's stream-ordered pool (eb_mem_in_use)."""
+    v = ctypes.c_int64(0)
+    _capi.check(_capi.lib().eb_mem_in_use(ctypes.byref(v)))
+    return v.value
+
+
+def _operand_shapes(einsum: str, dims) -> list:
+    ins = einsum.replace(" ", "").split("->")[0].split(",")
+    d = dict(dims) if not isinstance(dims, str) else {
+        kv.split("=")[0]: int(kv.split("=")[1]) for kv in dims.split(",") if kv}
+    return [tuple(int(d[c]) for c in t) for t in ins]
+
+
 def random_block(seed: int, gshape, base, shape, out: np.ndarray | None = None) -> np.ndarray:
     """The box [base, base+shape) of random_tensor(gshape, seed), generated
     without materialising the global tensor (into `out` when given, e.g. a
@@ -155,15 +205,19 @@ class Executor:
     """Rank-local GPU executor of an einplan schedule (eb_exec_*).
 
     ``rank=-1``: all ``procs`` ranks virtual on the current device.
-    ``rank>=0``: this process is one rank; ``nccl_id`` (128 bytes) comes from
-    :meth:`nccl_unique_id` on rank 0.
+    ``rank>=0``: this process is one rank; ``transport="nccl"`` (default)
+    takes ``nccl_id`` (128 bytes) from :meth:`nccl_unique_id` on rank 0;
+    ``transport="peer"`` meets the other ranks' processes in the POSIX
+    shared-memory segment ``group`` (e.g. "/eb_job42") and exchanges over
+    CUDA IPC peer memory — several processes may share one GPU.
     """
 
     def __init__(self, einsum: str, dims, procs: int = 1, fast_mem: float = 1024.0,
                  rank: int = -1, nccl_id: bytes | None = None, stream: int | None = None,
-                 like: "Executor | None" = None):
-        """``like=other``: same ranks and the same NCCL communicator as ``other``
-        (one ncclUniqueId initialises one communicator)."""
+                 like: "Executor | None" = None, transport: str = "nccl",
+                 group: str | None = None):
+        """``like=other``: same ranks and the same transport (communicator,
+        communication stream) as ``other``."""
         L = _capi.lib()
         self._h = ctypes.c_void_p()
         if like is not None:
@@ -172,14 +226,23 @@ class Executor:
                                               ctypes.byref(self._h)))
             procs, rank = like.procs, like.rank
             self._peer = like
+        elif rank >= 0 and transport == "peer":
+            if not group:
+                raise ValueError("Executor(transport='peer') needs a group name")
+            _capi.check(L.eb_exec_create_peer(einsum.encode(), dims_string(dims).encode(), procs,
+                                              fast_mem, rank, group.encode(),
+                                              ctypes.c_void_p(stream or 0), ctypes.byref(self._h)))
         else:
+            if transport not in ("nccl", "peer"):
+                raise ValueError(f"unknown transport {transport!r}")
             idbuf = (ctypes.create_string_buffer(bytes(nccl_id), 128)
                      if nccl_id is not None else None)
             _capi.check(L.eb_exec_create(einsum.encode(), dims_string(dims).encode(), procs,
                                          fast_mem, rank, idbuf, ctypes.c_void_p(stream or 0),
                                          ctypes.byref(self._h)))
         self.einsum, self.procs, self.rank = einsum, procs, rank
-        self.extents = dict(dims)
+        self.extents = dict(dims) if not isinstance(dims, str) else dims
+        self._shapes = _operand_shapes(einsum, dims)
         self._keep = None
 
     @staticmethod
@@ -202,7 +265,19 @@ class Executor:
     def stage(self, inputs: Sequence[np.ndarray | None]):
         """Copy host operands to this process's device blocks; ``None`` keeps an
         operand's device contents (e.g. one shared with :meth:`share_input`)."""
-        arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in inputs]
+        if len(inputs) != len(self._shapes):
+            raise ValueError(f"stage: {len(self._shapes)} operands expected, got {len(inputs)}")
+        arrs = []
+        for k, a in enumerate(inputs):
+            if a is None:
+                arrs.append(None)
+                continue
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            if a.size != int(np.prod(self._shapes[k])) or (
+                    a.ndim > 1 and tuple(a.shape) != self._shapes[k]):
+                raise ValueError(f"stage: operand {k} has shape {a.shape}, "
+                                 f"expected {self._shapes[k]}")
+            arrs.append(a)
         ptrs = (_capi._dp * len(arrs))(*[None if a is None else a.ctypes.data_as(_capi._dp)
                                           for a in arrs])
         _capi.check(_capi.lib().eb_exec_stage(self._h, ptrs))
@@ -217,10 +292,31 @@ class Executor:
 
     def stage_block(self, k: int, block: np.ndarray):
         """Stage operand k from a host array holding just this rank's box."""
+        _, shape = self.block(k)
         a = np.ascontiguousarray(block, dtype=np.float64)
+        if a.size != int(np.prod(shape)):
+            raise ValueError(f"stage_block: operand {k} box has {int(np.prod(shape))} elements, "
+                             f"got {a.size}")
         _capi.check(_capi.lib().eb_exec_stage_block(self._h, k, a.ctypes.data_as(_capi._dp)))
         self._keep_blocks = getattr(self, "_keep_blocks", {})
         self._keep_blocks[k] = a  # asynchronous copy: keep the source alive
+
+    def stage_region(self, k: int, base, region: np.ndarray) -> int:
+        """Virtual ranks: stage operand k's blocks that lie inside the global
+        sub-box [base, base + region.shape) from ``region`` (no global tensor
+        on the host).  Returns how many blocks were staged.  Synchronous."""
+        a = np.ascontiguousarray(region, dtype=np.float64)
+        nd = a.ndim
+        if nd != len(self._shapes[k]) or len(base) != nd:
+            raise ValueError("stage_region: region rank differs from the operand's")
+        arr = lambda v: (ctypes.c_int64 * nd)(*[int(x) for x in v])
+        n = ctypes.c_int(0)
+        _capi.check(_capi.lib().eb_exec_stage_region(self._h, k, arr(base), arr(a.shape), nd,
+                                                     a.ctypes.data_as(_capi._dp),
+                                                     ctypes.byref(n)))
+        import torch  # the copies read `a`: finish them before it may go away
+        torch.cuda.synchronize()
+        return n.value
 
     def share_input(self, k: int, src: "Executor", k_src: int):
         """Use ``src``'s staged device blocks for operand ``k`` (no copy)."""
@@ -246,10 +342,20 @@ class Executor:
         _capi.check(_capi.lib().eb_exec_run_pair(self._h, mode1._h, ctypes.byref(fused)))
         return bool(fused.value)
 
-    def gather(self, out: np.ndarray | None = None) -> np.ndarray:
-        n = _capi.lib().eb_exec_output_elems(self._h)
+    def output_elems(self) -> int:
+        return int(_capi.lib().eb_exec_output_elems(self._h))
+
+    def gather(self, out: np.ndarray | None = None) -> np.ndarray | None:
+        """The output on rank 0 (or in virtual mode); other ranks of a process
+        group take part (the call is collective) and get None."""
+        n = self.output_elems()
+        if self.rank > 0:
+            _capi.check(_capi.lib().eb_exec_gather(self._h, None))
+            return None
         if out is None:
             out = np.empty(n, dtype=np.float64)
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != n:
+            raise ValueError(f"gather: out must be a C-contiguous float64 array of {n} elements")
         _capi.check(_capi.lib().eb_exec_gather(self._h, out.ctypes.data_as(_capi._dp)))
         return out
 

@@ -58,7 +58,8 @@ EXPORTS = [
     "eb_last_error", "eb_build_info", "eb_contract_workspace", "eb_contract", "eb_mttkrp2_workspace", "eb_mttkrp2", "eb_ttm2",
     "eb_cp3_als_workspace", "eb_cp3_als_sweep",
     "eb_step_generic",
-    "eb_group_sum", "eb_copy_box", "eb_einsum_generic", "eb_random_fill_host",
+    "eb_group_sum", "eb_group_sum_into", "eb_copy_box", "eb_set_option", "eb_exec_create_peer",
+    "eb_exec_stage_region", "eb_rng_create", "eb_rng_fill", "eb_rng_destroy", "eb_mem_in_use", "eb_einsum_generic", "eb_random_fill_host",
     "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
@@ -134,6 +135,22 @@ def lib():
              [_vp, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
               ctypes.POINTER(ctypes.c_int)])
         _sig(L, "eb_exec_stage_block", ctypes.c_int, [_vp, ctypes.c_int, _dp])
+        _sig(L, "eb_exec_stage_region", ctypes.c_int,
+             [_vp, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.c_int, _dp,
+              ctypes.POINTER(ctypes.c_int)])
+        _sig(L, "eb_exec_create_peer", ctypes.c_int,
+             [c, c, _i64, ctypes.c_double, _i64, c, _vp, ctypes.POINTER(_vp)])
+        _sig(L, "eb_set_option", ctypes.c_int, [c, c])
+        _sig(L, "eb_group_sum", ctypes.c_int, [ctypes.POINTER(_dp), ctypes.c_int, _i64, _vp])
+        _sig(L, "eb_group_sum_into", ctypes.c_int,
+             [ctypes.POINTER(_dp), ctypes.c_int, _i64, _dp, _vp])
+        _sig(L, "eb_copy_box", ctypes.c_int,
+             [ctypes.c_int, _vp, ctypes.POINTER(_i64), _vp, ctypes.POINTER(_i64),
+              ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64), _vp])
+        _sig(L, "eb_rng_create", ctypes.c_int, [ctypes.c_uint64, _i64, ctypes.POINTER(_vp)])
+        _sig(L, "eb_rng_fill", None, [_vp, _dp, _i64])
+        _sig(L, "eb_rng_destroy", None, [_vp])
+        _sig(L, "eb_mem_in_use", ctypes.c_int, [ctypes.POINTER(_i64)])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,
              [c, c, _i64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(_vp)])

@@ -375,6 +375,20 @@ const char* eb_build_info(void) {
 
 void eb_free(void* p) { std::free(p); }
 
+int eb_mem_in_use(int64_t* bytes) {
+  return exec_guard([&] {
+    if (!bytes) throw eb::InvalidError("eb_mem_in_use: null argument");
+    int dev = 0;
+    cudaMemPool_t pool = nullptr;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess)
+      throw eb::DeviceError("eb_mem_in_use: no device");
+    std::uint64_t used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) != cudaSuccess)
+      throw eb::DeviceError("eb_mem_in_use: pool query failed");
+    *bytes = static_cast<int64_t>(used);
+  });
+}
+
 int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fast_mem,
                  int include_messages, char** json_out) {
   return exec_guard([&] {
@@ -416,6 +430,26 @@ int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double f
       throw eb::DeviceError("built without NCCL");
 #endif
     }
+    h->procs = procs;
+    h->exec = std::make_unique<gpu::ScheduleExecutor>(std::move(pipe), h->transport.get(),
+                                                      h->stream);
+    *out = h.release();
+  });
+}
+
+int eb_exec_create_peer(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                        int64_t rank, const char* group, void* stream, eb_exec** out) {
+  return exec_guard([&] {
+    if (!out || !group) throw eb::InvalidError("eb_exec_create_peer: null argument");
+    *out = nullptr;
+    if (rank < 0 || rank >= procs) throw eb::InvalidError("eb_exec_create_peer: rank outside 0..procs-1");
+    auto h = std::make_unique<eb_exec>();
+    h->fast_mem = fast_mem;
+    h->stream = static_cast<cudaStream_t>(stream);
+    Pipeline pipe = make_pipeline(make_spec(einsum, dims), procs, fast_mem);
+    auto shared = gpu::PeerShared::attach_shm(group, static_cast<int>(procs));
+    h->transport = std::make_shared<gpu::PeerTransport>(
+        std::make_shared<gpu::PeerComm>(shared, static_cast<int>(rank)), procs);
     h->procs = procs;
     h->exec = std::make_unique<gpu::ScheduleExecutor>(std::move(pipe), h->transport.get(),
                                                       h->stream);
@@ -465,6 +499,17 @@ int eb_exec_stage_block(eb_exec* h, int k, const double* host_block) {
   return exec_guard([&] {
     if (!h || !host_block) throw eb::InvalidError("eb_exec_stage_block: null argument");
     h->exec->stage_block(k, host_block);
+  });
+}
+
+int eb_exec_stage_region(eb_exec* h, int k, const int64_t* base, const int64_t* shape, int nd,
+                         const double* host_region, int* staged) {
+  return exec_guard([&] {
+    if (!h || !base || !shape || !host_region || nd < 0 || nd > 16)
+      throw eb::InvalidError("eb_exec_stage_region: bad argument");
+    const int n = h->exec->stage_region(k, std::vector<std::int64_t>(base, base + nd),
+                                        std::vector<std::int64_t>(shape, shape + nd), host_region);
+    if (staged) *staged = n;
   });
 }
 
@@ -537,6 +582,27 @@ int eb_exec_report_json(eb_exec* h, const double* host_out, char** json_out) {
     *json_out = heap_copy(run_report(h->exec->pipeline(), h->fast_mem, sim).dump(2));
   });
 }
+
+struct eb_rng {
+  std::mt19937_64 gen;
+};
+
+int eb_rng_create(uint64_t seed, int64_t skip, eb_rng** out) {
+  return eb::guard([&] {
+    if (!out || skip < 0) throw eb::InvalidError("eb_rng_create: bad argument");
+    auto g = std::make_unique<eb_rng>();
+    g->gen.seed(seed);
+    if (skip > 0) g->gen.discard(static_cast<unsigned long long>(skip));
+    *out = g.release();
+  });
+}
+
+void eb_rng_fill(eb_rng* g, double* out, int64_t n) {
+  for (int64_t k = 0; k < n; ++k)
+    out[k] = 2.0 * (static_cast<double>(g->gen() >> 11) * 0x1.0p-53) - 1.0;
+}
+
+void eb_rng_destroy(eb_rng* g) { delete g; }
 
 void eb_random_fill_host(double* out, int64_t n, uint64_t seed, int64_t skip) {
   std::mt19937_64 gen(seed);

@@ -341,6 +341,12 @@ struct SimulationReport {
   double tolerance = 0.0;
   bool pass = true;
   std::uint64_t seed = 0;
+  // B200 build: how the ranks ran ("virtual": every rank on one device;
+  // "devices": one host thread per GPU), on which devices, over which
+  // transport ("virtual", "peer", "nccl").  Reported as "execution".
+  std::string exec_mode;
+  std::vector<int> devices;
+  std::string transport;
 };
 
 struct RunOptions {

@@ -22,6 +22,8 @@
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <set>
+#include <thread>
 
 #include "status.hpp"
 
@@ -129,15 +131,47 @@ DeviceArena::~DeviceArena() {
 
 // ------------------------------------------------------- transports --
 
+Transport::~Transport() {
+  if (comm_stream_) {
+    cudaStreamSynchronize(comm_stream_);
+    cudaStreamDestroy(comm_stream_);
+  }
+}
+
+cudaStream_t Transport::comm_stream() {
+  if (!comm_stream_)
+    cuda_ok(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+  return comm_stream_;
+}
+
+namespace {
+
+// Reduction groups of a placement: ranks holding the same output block
+// (executor.cpp:84-86), ascending; accounts the reference's volumes
+// (elements x (group - 1), per-rank sends, executor.cpp:103-105).
+std::map<std::vector<std::int64_t>, std::vector<std::int64_t>> reduction_groups(
+    const TensorPlacement& place, std::vector<std::int64_t>& per_rank_sent, std::int64_t& volume) {
+  std::map<std::vector<std::int64_t>, std::vector<std::int64_t>> groups;
+  const std::int64_t procs = place.term_grid.total();
+  for (std::int64_t r = 0; r < procs; ++r) groups[place.block_coords_of(r)].push_back(r);
+  volume = 0;
+  for (auto& kv : groups) {
+    const std::int64_t n = prod(place.dist.shape_of(kv.first));
+    for (std::int64_t r : kv.second) per_rank_sent[static_cast<std::size_t>(r)] += n;
+    volume += n * (static_cast<std::int64_t>(kv.second.size()) - 1);
+  }
+  return groups;
+}
+
+}  // namespace
+
 std::int64_t VirtualTransport::allreduce(const TensorPlacement& place, const ReductionGroup& grp,
                                          std::vector<DevBlock>& blocks,
                                          std::vector<std::int64_t>& per_rank_sent,
                                          cudaStream_t st) {
   if (grp.depth <= 1) return 0;
-  std::map<std::vector<std::int64_t>, std::vector<std::int64_t>> groups;
-  const std::int64_t procs = place.term_grid.total();
-  for (std::int64_t r = 0; r < procs; ++r) groups[place.block_coords_of(r)].push_back(r);
   std::int64_t volume = 0;
+  const auto groups = reduction_groups(place, per_rank_sent, volume);
   for (auto& kv : groups) {
     const auto& members = kv.second;
     std::vector<double*> ptrs;
@@ -150,8 +184,6 @@ std::int64_t VirtualTransport::allreduce(const TensorPlacement& place, const Red
       ptrs.push_back(b.ptr);
     }
     eb_ok(eb_group_sum(ptrs.data(), static_cast<int>(ptrs.size()), n, st), "eb_group_sum");
-    for (std::int64_t r : members) per_rank_sent[static_cast<std::size_t>(r)] += n;
-    volume += n * (static_cast<std::int64_t>(members.size()) - 1);
   }
   return volume;
 }
@@ -169,6 +201,85 @@ void VirtualTransport::redistribute(const RedistributionPlan& plan,
                       d.shape.data(), m.oy_lo.data(), m.oy_hi.data(), m.ox_lo.data(), st),
           "eb_copy_box");
   }
+}
+
+// ---- peer memory ----
+
+PeerTransport::PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks)
+    : comm_(std::move(comm)), nranks_(nranks) {
+  if (comm_->nranks() != nranks)
+    fail(errc::invalid_argument, "peer transport: group of " + std::to_string(comm_->nranks()) +
+                                     " ranks for a schedule of " + std::to_string(nranks));
+}
+
+std::int64_t PeerTransport::allreduce(const TensorPlacement& place, const ReductionGroup& grp,
+                                      std::vector<DevBlock>& blocks,
+                                      std::vector<std::int64_t>& per_rank_sent, cudaStream_t st) {
+  if (grp.depth <= 1) return 0;
+  std::int64_t volume = 0;
+  const auto groups = reduction_groups(place, per_rank_sent, volume);
+  const std::int64_t me = comm_->rank();
+  const auto& members = groups.at(place.block_coords_of(me));
+  DevBlock& mine = blocks[static_cast<std::size_t>(me)];
+  const std::int64_t n = mine.size();
+  std::vector<const double*> ptrs;
+  for (std::int64_t r : members) {
+    const DevBlock& b = blocks[static_cast<std::size_t>(r)];
+    if (!b.ptr || b.size() != n)
+      fail(errc::invalid_argument,
+           "allreduce: rank " + std::to_string(r) + " block of \"" + place.tensor + "\" not mapped");
+    ptrs.push_back(b.ptr);
+  }
+  cuda_ok(cudaStreamSynchronize(st), "allreduce: sync");
+  comm_->barrier();  // every partial of every group is complete
+  double* sum = nullptr;
+  if (n > 0 && members.size() > 1) {
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&sum), static_cast<std::size_t>(n) * 8, st),
+            "allreduce: scratch");
+    eb_ok(eb_group_sum_into(ptrs.data(), static_cast<int>(ptrs.size()), n, sum, st),
+          "eb_group_sum_into");
+  }
+  cuda_ok(cudaStreamSynchronize(st), "allreduce: sync");
+  comm_->barrier();  // every member has read every partial: overwrite own block
+  if (sum) {
+    cuda_ok(cudaMemcpyAsync(mine.ptr, sum, static_cast<std::size_t>(n) * 8,
+                            cudaMemcpyDeviceToDevice, st),
+            "allreduce: write back");
+    cuda_ok(cudaFreeAsync(sum, st), "allreduce: scratch");
+  }
+  // readers of the sum (a redistribution, the gather) start with a sync +
+  // barrier of their own, after which this write is complete
+  return volume;
+}
+
+void PeerTransport::redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
+                                 std::vector<DevBlock>& dst, cudaStream_t st) {
+  const std::int64_t me = comm_->rank();
+  cuda_ok(cudaStreamSynchronize(st), "redistribute: sync");
+  comm_->barrier();  // every source block is complete
+  DevBlock& d = dst[static_cast<std::size_t>(me)];
+  for (const Message& m : plan.messages) {
+    if (m.dst_rank != me) continue;
+    const DevBlock& s = src[static_cast<std::size_t>(m.src_rank)];
+    if (!s.ptr && m.elements > 0)
+      fail(errc::invalid_argument,
+           "apply_plan: source block of rank " + std::to_string(m.src_rank) + " not mapped");
+    eb_ok(eb_copy_box(static_cast<int>(m.oy_lo.size()), s.ptr, s.shape.data(), d.ptr,
+                      d.shape.data(), m.oy_lo.data(), m.oy_hi.data(), m.ox_lo.data(), st),
+          "eb_copy_box (peer pull)");
+  }
+  cuda_ok(cudaStreamSynchronize(st), "redistribute: sync");
+  comm_->barrier();  // every destination has pulled: sources may be reused
+}
+
+void PeerTransport::gather_to_root(const TensorPlacement&, std::vector<DevBlock>&, cudaStream_t st) {
+  cuda_ok(cudaStreamSynchronize(st), "gather: sync");
+  comm_->barrier();  // canonical blocks final; rank 0 reads them from the peers' heaps
+}
+
+void PeerTransport::gather_done(std::vector<DevBlock>&, cudaStream_t st) {
+  cuda_ok(cudaStreamSynchronize(st), "gather: sync");
+  comm_->barrier();
 }
 
 #ifdef EB_HAVE_NCCL
@@ -190,9 +301,31 @@ NcclTransport::NcclTransport(const void* unique_id, std::int64_t nranks, std::in
   world_ = c;
 }
 
+NcclTransport::NcclTransport(void* comm, std::int64_t nranks, std::int64_t rank)
+    : rank_(rank), nranks_(nranks), world_(comm) {}
+
 NcclTransport::~NcclTransport() {
+  if (staging_done_) cudaEventSynchronize(staging_done_);
+  if (staging_) cudaFree(staging_);
+  if (staging_done_) cudaEventDestroy(staging_done_);
   for (auto& kv : split_) ncclCommDestroy(static_cast<ncclComm_t>(kv.second));
   if (world_) ncclCommDestroy(static_cast<ncclComm_t>(world_));
+}
+
+double* NcclTransport::staging(std::int64_t elems, cudaStream_t st) {
+  if (!staging_done_)
+    cuda_ok(cudaEventCreateWithFlags(&staging_done_, cudaEventDisableTiming), "event");
+  else
+    cuda_ok(cudaStreamWaitEvent(st, staging_done_, 0), "staging: wait for its last use");
+  if (elems > staging_elems_) {
+    if (staging_) cuda_ok(cudaFreeAsync(staging_, st), "staging free");
+    staging_ = nullptr;
+    cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&staging_),
+                            static_cast<std::size_t>(elems) * 8, st),
+            "staging alloc");
+    staging_elems_ = elems;
+  }
+  return staging_;
 }
 
 std::int64_t NcclTransport::allreduce(const TensorPlacement& place, const ReductionGroup& grp,
@@ -200,18 +333,12 @@ std::int64_t NcclTransport::allreduce(const TensorPlacement& place, const Reduct
                                       std::vector<std::int64_t>& per_rank_sent, cudaStream_t st) {
   if (grp.depth <= 1) return 0;
   // Group = ranks holding the same output block; color it by the block's
-  // linear coordinate so ncclCommSplit reproduces executor.cpp:84-86.
-  std::map<std::vector<std::int64_t>, std::vector<std::int64_t>> groups;
-  const std::int64_t procs = place.term_grid.total();
-  for (std::int64_t r = 0; r < procs; ++r) groups[place.block_coords_of(r)].push_back(r);
-  const auto mine = place.block_coords_of(rank_);
-  int color = 0;
+  // index among the groups so ncclCommSplit reproduces executor.cpp:84-86.
   std::int64_t volume = 0;
-  int idx = 0;
+  const auto groups = reduction_groups(place, per_rank_sent, volume);
+  const auto mine = place.block_coords_of(rank_);
+  int color = 0, idx = 0;
   for (auto& kv : groups) {
-    const std::int64_t n = prod(place.dist.shape_of(kv.first));
-    for (std::int64_t r : kv.second) per_rank_sent[static_cast<std::size_t>(r)] += n;
-    volume += n * (static_cast<std::int64_t>(kv.second.size()) - 1);
     if (kv.first == mine) color = idx;
     ++idx;
   }
@@ -236,44 +363,48 @@ std::int64_t NcclTransport::allreduce(const TensorPlacement& place, const Reduct
 
 void NcclTransport::redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
                                  std::vector<DevBlock>& dst, cudaStream_t st) {
-  // Pack every outgoing box, exchange with grouped point-to-point calls,
-  // unpack every incoming box; self messages copy in place.
+  // Pack every outgoing box into one reused staging buffer, exchange with
+  // grouped point-to-point calls, unpack every incoming box; self messages
+  // copy in place.
   struct Pending {
     const Message* m;
-    double* buf;
+    std::int64_t off;
   };
   std::vector<Pending> sends, recvs;
+  std::int64_t total = 0;
   for (const Message& m : plan.messages) {
     if (m.src_rank != rank_ && m.dst_rank != rank_) continue;
-    if (m.src_rank == rank_ && m.dst_rank == rank_) {
-      const DevBlock& s = src[static_cast<std::size_t>(rank_)];
-      DevBlock& d = dst[static_cast<std::size_t>(rank_)];
-      eb_ok(eb_copy_box(static_cast<int>(m.oy_lo.size()), s.ptr, s.shape.data(), d.ptr,
-                        d.shape.data(), m.oy_lo.data(), m.oy_hi.data(), m.ox_lo.data(), st),
-            "eb_copy_box");
-      continue;
-    }
-    double* buf = arena_.alloc(m.elements, st, false);
+    if (m.src_rank == rank_ && m.dst_rank == rank_) continue;
+    (m.src_rank == rank_ ? sends : recvs).push_back({&m, total});
+    total += m.elements;
+  }
+  double* buf = total > 0 ? staging(total, st) : nullptr;
+  for (const Message& m : plan.messages) {
+    if (m.src_rank != rank_ || m.dst_rank != rank_) continue;
+    const DevBlock& s = src[static_cast<std::size_t>(rank_)];
+    DevBlock& d = dst[static_cast<std::size_t>(rank_)];
+    eb_ok(eb_copy_box(static_cast<int>(m.oy_lo.size()), s.ptr, s.shape.data(), d.ptr,
+                      d.shape.data(), m.oy_lo.data(), m.oy_hi.data(), m.ox_lo.data(), st),
+          "eb_copy_box");
+  }
+  if (total == 0) return;
+  for (auto& p : sends) {
+    const Message& m = *p.m;
     const std::size_t nd = m.oy_lo.size();
     std::vector<std::int64_t> box(nd), zeros(nd, 0);
     for (std::size_t d = 0; d < nd; ++d) box[d] = m.oy_hi[d] - m.oy_lo[d];
-    if (m.src_rank == rank_) {
-      const DevBlock& s = src[static_cast<std::size_t>(rank_)];
-      eb_ok(eb_copy_box(static_cast<int>(nd), s.ptr, s.shape.data(), buf, box.data(),
-                        m.oy_lo.data(), m.oy_hi.data(), zeros.data(), st),
-            "pack");
-      sends.push_back({&m, buf});
-    } else {
-      recvs.push_back({&m, buf});
-    }
+    const DevBlock& s = src[static_cast<std::size_t>(rank_)];
+    eb_ok(eb_copy_box(static_cast<int>(nd), s.ptr, s.shape.data(), buf + p.off, box.data(),
+                      m.oy_lo.data(), m.oy_hi.data(), zeros.data(), st),
+          "pack");
   }
   nccl_ok(ncclGroupStart(), "ncclGroupStart");
   for (auto& p : sends)
-    nccl_ok(ncclSend(p.buf, static_cast<std::size_t>(p.m->elements), ncclFloat64,
+    nccl_ok(ncclSend(buf + p.off, static_cast<std::size_t>(p.m->elements), ncclFloat64,
                      static_cast<int>(p.m->dst_rank), static_cast<ncclComm_t>(world_), st),
             "ncclSend");
   for (auto& p : recvs)
-    nccl_ok(ncclRecv(p.buf, static_cast<std::size_t>(p.m->elements), ncclFloat64,
+    nccl_ok(ncclRecv(buf + p.off, static_cast<std::size_t>(p.m->elements), ncclFloat64,
                      static_cast<int>(p.m->src_rank), static_cast<ncclComm_t>(world_), st),
             "ncclRecv");
   nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
@@ -283,16 +414,17 @@ void NcclTransport::redistribute(const RedistributionPlan& plan, const std::vect
     std::vector<std::int64_t> box(nd), zeros(nd, 0);
     for (std::size_t d = 0; d < nd; ++d) box[d] = m.oy_hi[d] - m.oy_lo[d];
     DevBlock& d = dst[static_cast<std::size_t>(rank_)];
-    eb_ok(eb_copy_box(static_cast<int>(nd), p.buf, box.data(), d.ptr, d.shape.data(),
+    eb_ok(eb_copy_box(static_cast<int>(nd), buf + p.off, box.data(), d.ptr, d.shape.data(),
                       zeros.data(), box.data(), m.ox_lo.data(), st),
           "unpack");
   }
+  cuda_ok(cudaEventRecord(staging_done_, st), "event record");
 }
 
 void NcclTransport::gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
                                    cudaStream_t st) {
   // Canonical owners send their block to rank 0, which receives every
-  // non-local canonical block into its own staging buffers.
+  // non-local canonical block into buffers released by gather_done().
   const std::int64_t procs = place.term_grid.total();
   nccl_ok(ncclGroupStart(), "ncclGroupStart");
   for (std::int64_t r = 1; r < procs; ++r) {
@@ -304,13 +436,28 @@ void NcclTransport::gather_to_root(const TensorPlacement& place, std::vector<Dev
               "ncclSend");
     if (rank_ == 0) {
       DevBlock& b = blocks[static_cast<std::size_t>(r)];
-      if (!b.ptr) b.ptr = arena_.alloc(n, st, false);
+      double* p = nullptr;
+      cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&p),
+                              static_cast<std::size_t>(std::max<std::int64_t>(n, 1)) * 8, st),
+              "gather buffer");
+      gathered_.push_back(p);
+      b.ptr = p;
       nccl_ok(ncclRecv(b.ptr, static_cast<std::size_t>(n), ncclFloat64, static_cast<int>(r),
                        static_cast<ncclComm_t>(world_), st),
               "ncclRecv");
     }
   }
   nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+void NcclTransport::gather_done(std::vector<DevBlock>& blocks, cudaStream_t st) {
+  if (gathered_.empty()) return;
+  for (double* p : gathered_) {
+    for (DevBlock& b : blocks)
+      if (b.ptr == p) b.ptr = nullptr;
+    cudaFreeAsync(p, st);
+  }
+  gathered_.clear();
 }
 
 #endif  // EB_HAVE_NCCL
@@ -336,16 +483,16 @@ ScheduleExecutor::ScheduleExecutor(Pipeline pipe, Transport* transport, cudaStre
 ScheduleExecutor::~ScheduleExecutor() {
   if (comm_pending_) cudaStreamWaitEvent(stream_, ev_comm_, 0);  // no throwing in a destructor
   cudaStreamSynchronize(stream_);
-  if (comm_stream_) {
-    cudaStreamSynchronize(comm_stream_);
-    cudaStreamDestroy(comm_stream_);
-  }
   if (ev_compute_) cudaEventDestroy(ev_compute_);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   run_arena_.release(stream_);
   input_arena_.release(stream_);
   cudaFreeAsync(workspace_, stream_);
   cudaStreamSynchronize(stream_);
+  if (heap_) {
+    if (auto* pt = dynamic_cast<PeerTransport*>(transport_)) pt->comm().unmap(heap_peers_);
+    cudaFree(heap_);
+  }
 }
 
 std::int64_t ScheduleExecutor::local_lo(const TermPlan& t, char c, std::int64_t rank) const {
@@ -445,6 +592,59 @@ void ScheduleExecutor::stage_block(int k, const double* host_block) {
     for (const AccessArray& arr : term.statement.arrays)
       if (arr.tensor.rfind("in", 0) == 0 && !inputs_.count({term.index, arr.tensor})) all = false;
   staged_ = all;
+}
+
+int ScheduleExecutor::stage_region(int k, const std::vector<std::int64_t>& rbase,
+                                   const std::vector<std::int64_t>& rshape, const double* host) {
+  const auto& spec = pipe_.spec;
+  if (k < 0 || static_cast<std::size_t>(k) >= spec.inputs.size())
+    fail(errc::invalid_argument, "stage_region: no operand " + std::to_string(k));
+  const std::string name = "in" + std::to_string(k);
+  const auto gshape = spec.shape_of(spec.inputs[static_cast<std::size_t>(k)]);
+  if (rbase.size() != gshape.size() || rshape.size() != gshape.size())
+    fail(errc::invalid_argument, "stage_region: region rank differs from the operand's");
+  for (std::size_t d = 0; d < gshape.size(); ++d)
+    if (rbase[d] < 0 || rshape[d] < 0 || rbase[d] + rshape[d] > gshape[d])
+      fail(errc::invalid_argument, "stage_region: region outside the operand");
+  int staged = 0;
+  for (const TermPlan& term : pipe_.schedule.terms)
+    for (const AccessArray& arr : term.statement.arrays) {
+      if (arr.tensor != name) continue;
+      const auto key = std::make_pair(term.index, name);
+      if (aliased_.count(key))
+        fail(errc::invalid_argument, "stage_region: " + name + " is shared from another executor");
+      const TensorPlacement& place = term.placement_of(name);
+      auto it = inputs_.find(key);
+      if (it == inputs_.end()) {
+        std::vector<DevBlock> blocks(static_cast<std::size_t>(pipe_.schedule.procs));
+        for (std::int64_t r : owned_) {
+          DevBlock& b = blocks[static_cast<std::size_t>(r)];
+          const auto bc = place.block_coords_of(r);
+          b.base = place.dist.base_of(bc);
+          b.shape = place.dist.shape_of(bc);
+          b.ptr = input_arena_.alloc(prod(b.shape), stream_, false);
+        }
+        it = inputs_.emplace(key, std::move(blocks)).first;
+      }
+      for (std::int64_t r : owned_) {
+        const DevBlock& b = it->second[static_cast<std::size_t>(r)];
+        bool inside = true;
+        std::vector<std::int64_t> rel(b.base.size());
+        for (std::size_t d = 0; d < b.base.size(); ++d) {
+          rel[d] = b.base[d] - rbase[d];
+          inside = inside && rel[d] >= 0 && rel[d] + b.shape[d] <= rshape[d];
+        }
+        if (!inside) continue;
+        copy_box_host(true, const_cast<double*>(host), rshape, b.shape, rel, b.ptr, stream_);
+        ++staged;
+      }
+    }
+  bool all = true;
+  for (const TermPlan& term : pipe_.schedule.terms)
+    for (const AccessArray& arr : term.statement.arrays)
+      if (arr.tensor.rfind("in", 0) == 0 && !inputs_.count({term.index, arr.tensor})) all = false;
+  staged_ = all;
+  return staged;
 }
 
 void ScheduleExecutor::share_input(int k, const ScheduleExecutor& src, int k_src) {
@@ -554,14 +754,75 @@ MttkrpMatch match_mttkrp(const FusedStatement& st) {
 }  // namespace
 
 DevBlock ScheduleExecutor::new_block(const TermPlan& term, const std::string& idx,
-                                     std::int64_t rank, bool zero) {
+                                     std::int64_t rank, bool zero, bool is_output) {
   DevBlock b;
   for (char c : idx) {
     b.shape.push_back(local_len(term, c, rank));
     b.base.push_back(local_lo(term, c, rank));
   }
-  b.ptr = run_arena_.alloc(prod(b.shape), stream_, zero);
+  const auto slot = heap_slot_.find(term.index);
+  if (is_output && heap_ && slot != heap_slot_.end()) {
+    b.ptr = reinterpret_cast<double*>(heap_ + slot->second);
+    if (zero)
+      cuda_ok(cudaMemsetAsync(b.ptr, 0, static_cast<std::size_t>(prod(b.shape)) * 8, stream_),
+              "cudaMemsetAsync");
+  } else {
+    b.ptr = run_arena_.alloc(prod(b.shape), stream_, zero);
+  }
   return b;
+}
+
+void ScheduleExecutor::prepare_heap() {
+  if (!transport_->peer_mapped()) return;
+  auto* pt = static_cast<PeerTransport*>(transport_);
+  const auto& terms = pipe_.schedule.terms;
+  const std::int64_t procs = pipe_.schedule.procs;
+  heap_slot_.clear();
+  std::size_t off = 0;
+  for (const TermPlan& t : terms) {
+    bool leaves = t.reduction.depth > 1 || &t == &terms.back();
+    for (const RedistRecord& rec : pipe_.schedule.redistributions)
+      if (rec.from_term == t.index && rec.tensor == t.statement.output) leaves = true;
+    if (!leaves) continue;
+    const std::string& idx = t.placement_of(t.statement.output).indices;
+    std::int64_t most = 1;
+    for (std::int64_t r = 0; r < procs; ++r) {
+      std::int64_t n = 1;
+      for (char c : idx) n *= local_len(t, c, r);
+      most = std::max(most, n);
+    }
+    heap_slot_[t.index] = off;
+    off += (static_cast<std::size_t>(most) * 8 + 255) / 256 * 256;
+  }
+  // identical on every rank (same schedule), so the decision is collective
+  if (off <= heap_bytes_) return;
+  cuda_ok(cudaStreamSynchronize(stream_), "heap: sync");
+  pt->comm().unmap(heap_peers_);
+  pt->comm().barrier();  // no rank maps the old heaps any more
+  if (heap_) cuda_ok(cudaFree(heap_), "heap free");
+  heap_ = nullptr;
+  heap_bytes_ = 0;
+  cuda_ok(cudaMalloc(reinterpret_cast<void**>(&heap_), off), "exchange heap");
+  heap_bytes_ = off;
+  heap_peers_ = pt->comm().exchange(heap_);
+}
+
+void ScheduleExecutor::map_peer_blocks(const TermPlan& term, std::vector<DevBlock>& blocks) {
+  const auto slot = heap_slot_.find(term.index);
+  if (!heap_ || slot == heap_slot_.end()) return;
+  const std::string& idx = term.placement_of(term.statement.output).indices;
+  for (std::int64_t r = 0; r < pipe_.schedule.procs; ++r) {
+    if (transport_->owns(r)) continue;
+    DevBlock& b = blocks[static_cast<std::size_t>(r)];
+    b.shape.clear();
+    b.base.clear();
+    for (char c : idx) {
+      b.shape.push_back(local_len(term, c, r));
+      b.base.push_back(local_lo(term, c, r));
+    }
+    char* base = heap_peers_[static_cast<std::size_t>(r)];
+    b.ptr = base ? reinterpret_cast<double*>(base + slot->second) : nullptr;
+  }
 }
 
 bool ScheduleExecutor::try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
@@ -614,7 +875,7 @@ bool ScheduleExecutor::try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
     d.ldu = u.ld;
   }
   if (d.n_pre > 8 || d.n_mid > 8) return false;
-  out = new_block(term, term.placement_of(term.statement.output).indices, rank, false);
+  out = new_block(term, term.placement_of(term.statement.output).indices, rank, false, true);
   d.out = out.ptr;
   const std::size_t wb = eb_contract_workspace(&d);
   if (wb == 0) return false;
@@ -668,7 +929,7 @@ bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
   d.ldu1 = u1->shape[1];
   d.U2 = u2->ptr;
   d.ldu2 = u2->shape[1];
-  out = new_block(term, s1.result_indices, rank, false);
+  out = new_block(term, s1.result_indices, rank, false, true);
   d.out = out.ptr;
   eb_ok(eb_ttm2(&d, stream_), "eb_ttm2 (fused TTM pair)");
   ++launches_fused_;
@@ -686,7 +947,9 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
            "local_contract: missing operand block \"" + tree.tensor_name(id) + "\"");
     return it->second;
   };
-  DevBlock out = new_block(term, s.result_indices, rank, false);
+  const bool is_output =
+      tree.tensor_name(tree.result_id(sid)) == term.statement.output;
+  DevBlock out = new_block(term, s.result_indices, rank, false, is_output);
   const DevBlock* lhs = operand(s.lhs);
   const DevBlock* rhs = s.rhs >= 0 ? operand(s.rhs) : nullptr;
 
@@ -758,16 +1021,18 @@ std::int64_t ScheduleExecutor::reduce(const TensorPlacement& place, const Reduct
                                       std::vector<DevBlock>& blocks, bool last_term) {
   if (!async_reduce_ || grp.depth <= 1)
     return transport_->allreduce(place, grp, blocks, comm_.per_rank_sent, stream_);
-  if (!comm_stream_) {
-    cuda_ok(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+  // the transport's one communication stream: every executor of this
+  // process issues its collectives there, in program order
+  cudaStream_t cs = transport_->comm_stream();
+  if (!ev_compute_) {
     cuda_ok(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming), "event");
     cuda_ok(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming), "event");
   }
   join();  // one reduction in flight per executor
   cuda_ok(cudaEventRecord(ev_compute_, stream_), "event record");
-  cuda_ok(cudaStreamWaitEvent(comm_stream_, ev_compute_, 0), "stream wait");
-  const std::int64_t v = transport_->allreduce(place, grp, blocks, comm_.per_rank_sent, comm_stream_);
-  cuda_ok(cudaEventRecord(ev_comm_, comm_stream_), "event record");
+  cuda_ok(cudaStreamWaitEvent(cs, ev_compute_, 0), "stream wait");
+  const std::int64_t v = transport_->allreduce(place, grp, blocks, comm_.per_rank_sent, cs);
+  cuda_ok(cudaEventRecord(ev_comm_, cs), "event record");
   comm_pending_ = true;
   if (!last_term) join();  // the next term reads it on the compute stream
   return v;
@@ -782,6 +1047,7 @@ void ScheduleExecutor::execute() {
   comm_.per_rank_sent.assign(static_cast<std::size_t>(pipe_.schedule.procs), 0);
   launches_fused_ = launches_ttm_ = launches_generic_ = 0;
   const std::int64_t procs = pipe_.schedule.procs;
+  prepare_heap();
 
   for (const TermPlan& term : pipe_.schedule.terms) {
     std::map<std::string, std::vector<DevBlock>*> arrays;
@@ -828,7 +1094,9 @@ void ScheduleExecutor::execute() {
         todo.messages.clear();
         for (const Message& m : rec->plan.messages)
           if (!(m.self && alias[static_cast<std::size_t>(m.dst_rank)])) todo.messages.push_back(m);
-        if (!todo.messages.empty()) transport_->redistribute(todo, src, dst, stream_);
+        // (collective for the peer transport: its barriers need every rank)
+        if (!todo.messages.empty() || transport_->peer_mapped())
+          transport_->redistribute(todo, src, dst, stream_);
         comm_.events.push_back(
             {"redistribute", term.index, a.tensor, rec->plan.transmitted_volume});
         comm_.redistribute_volume += rec->plan.transmitted_volume;
@@ -853,7 +1121,7 @@ void ScheduleExecutor::execute() {
       for (auto& kv : arrays) at_hand[kv.first] = &(*kv.second)[static_cast<std::size_t>(rank)];
       DevBlock result;
       if (try_fused_mttkrp(term, rank, at_hand, result) ||
-          (fuse_ttm_ && try_fused_ttm2(term, rank, at_hand, result))) {
+          (eb::options().fuse_ttm2 && try_fused_ttm2(term, rank, at_hand, result))) {
         out_blocks[static_cast<std::size_t>(rank)] = result;
         continue;
       }
@@ -869,6 +1137,7 @@ void ScheduleExecutor::execute() {
         }
       }
     }
+    map_peer_blocks(term, out_blocks);
     const std::int64_t v = reduce(out_place, term.reduction, out_blocks,
                                   &term == &pipe_.schedule.terms.back());
     if (term.reduction.depth > 1) {
@@ -938,6 +1207,7 @@ bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
 
   for (ScheduleExecutor* e : {this, &m1}) {
     e->join();
+    e->prepare_heap();
     e->run_arena_.release(e->stream_);
     e->store_.clear();
     e->comm_ = CommStats{};
@@ -950,8 +1220,8 @@ bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
   for (std::int64_t r : owned_) {
     eb_contract_desc& d = descs[k++];
     const auto i = static_cast<std::size_t>(r);
-    out0[i] = new_block(t0, t0.placement_of(t0.statement.output).indices, r, false);
-    out1[i] = m1.new_block(t1, t1.placement_of(t1.statement.output).indices, r, false);
+    out0[i] = new_block(t0, t0.placement_of(t0.statement.output).indices, r, false, true);
+    out1[i] = m1.new_block(t1, t1.placement_of(t1.statement.output).indices, r, false, true);
     d.out = out0[i].ptr;
     const std::size_t wb = eb_mttkrp2_workspace(&d);
     eb_ok(eb_mttkrp2(&d, (*af)[i].ptr, (*af)[i].shape[1], out1[i].ptr, workspace(wb), wb, stream_),
@@ -963,6 +1233,8 @@ bool ScheduleExecutor::execute_pair(ScheduleExecutor& m1) {
     const TermPlan* t;
     std::vector<DevBlock>* out;
   };
+  map_peer_blocks(t0, out0);
+  m1.map_peer_blocks(t1, out1);
   for (const Side& sd : {Side{this, &t0, &out0}, Side{&m1, &t1, &out1}}) {
     const TensorPlacement& place = sd.t->placement_of(sd.t->statement.output);
     const std::int64_t v = sd.e->reduce(place, sd.t->reduction, *sd.out, true);
@@ -987,8 +1259,10 @@ void ScheduleExecutor::gather(double* host_out) {
   transport_->gather_to_root(place, blocks, stream_);
   if (!transport_->owns(0) && !transport_->is_virtual()) {
     cuda_ok(cudaStreamSynchronize(stream_), "sync");
+    transport_->gather_done(blocks, stream_);
     return;  // only rank 0 assembles
   }
+  if (!host_out) fail(errc::invalid_argument, "gather: rank 0 needs an output buffer");
   const auto gshape = place.dist.extents;
   const std::int64_t procs = place.term_grid.total();
   for (std::int64_t r = 0; r < procs; ++r) {
@@ -996,9 +1270,12 @@ void ScheduleExecutor::gather(double* host_out) {
     const DevBlock& b = blocks[static_cast<std::size_t>(r)];
     const auto shape = place.dist.shape_of(place.block_coords_of(r));
     const auto base = place.dist.base_of(place.block_coords_of(r));
+    if (!b.ptr) fail(errc::invalid_argument, "gather: canonical block of rank " +
+                                                 std::to_string(r) + " not available");
     copy_box_host(false, host_out, gshape, shape, base, b.ptr, stream_);
   }
   cuda_ok(cudaStreamSynchronize(stream_), "sync");
+  transport_->gather_done(blocks, stream_);
 }
 
 void ScheduleExecutor::verify(const std::vector<const double*>& globals, const double* host_out,
@@ -1042,8 +1319,177 @@ void ScheduleExecutor::verify(const std::vector<const double*>& globals, const d
 
 }  // namespace gpu
 
-// The reference's C++ entry point, executed on the current GPU with every
-// virtual rank resident on it.
+namespace {
+
+// How einplan::run / einplan_run_json place the ranks (procs =
+// GPU count).  Runtime configuration of the outer ABI, read per call like the
+// reference's EINPLAN_MAX_POINTS (capi.cpp:80-87):
+//   EINPLAN_EXEC      "virtual" forces every rank onto the current device;
+//   EINPLAN_DEVICES   "d0,d1,..." explicit rank -> device map (cycled), e.g.
+//                     "0,0" runs two rank threads on one GPU (peer transport);
+//   EINPLAN_TRANSPORT "nccl" | "peer" for the one-thread-per-GPU mode.
+// Default: one host thread per GPU on devices 0..procs-1 when procs <= the
+// visible GPU count (NCCL when the devices are distinct), else virtual ranks.
+struct ExecChoice {
+  bool threads = false;
+  std::vector<int> dev;
+  std::string transport = "virtual";
+};
+
+ExecChoice choose_execution(std::int64_t procs) {
+  ExecChoice c;
+  const char* mode = std::getenv("EINPLAN_EXEC");
+  if (mode && std::string(mode) == "virtual") return c;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    ndev = 0;
+  }
+  std::vector<int> list;
+  if (const char* v = std::getenv("EINPLAN_DEVICES")) {
+    std::string s(v);
+    std::size_t pos = 0;
+    while (pos <= s.size()) {
+      const std::size_t q = s.find(',', pos);
+      const std::string item = s.substr(pos, q == std::string::npos ? std::string::npos : q - pos);
+      if (!item.empty()) {
+        const int d = std::atoi(item.c_str());
+        if (d < 0 || d >= ndev)
+          fail(errc::invalid_argument, "EINPLAN_DEVICES: no device " + item);
+        list.push_back(d);
+      }
+      if (q == std::string::npos) break;
+      pos = q + 1;
+    }
+  }
+  if (list.empty()) {
+    if (procs > ndev || procs > gpu::kMaxPeers) return c;  // more ranks than GPUs: virtual
+    for (int r = 0; r < procs; ++r) list.push_back(r);
+  }
+  if (procs > gpu::kMaxPeers) fail(errc::invalid_argument, "run: at most 64 rank threads");
+  c.threads = true;
+  for (std::int64_t r = 0; r < procs; ++r) c.dev.push_back(list[static_cast<std::size_t>(r) % list.size()]);
+  const std::set<int> distinct(c.dev.begin(), c.dev.end());
+  c.transport = "peer";
+#ifdef EB_HAVE_NCCL
+  if (procs > 1 && distinct.size() == c.dev.size()) c.transport = "nccl";
+#endif
+  if (const char* t = std::getenv("EINPLAN_TRANSPORT")) {
+    const std::string ts(t);
+    if (ts == "peer") {
+      c.transport = "peer";
+    } else if (ts == "nccl") {
+#ifndef EB_HAVE_NCCL
+      fail(errc::invalid_argument, "EINPLAN_TRANSPORT=nccl: built without NCCL");
+#endif
+      if (distinct.size() != c.dev.size())
+        fail(errc::invalid_argument, "EINPLAN_TRANSPORT=nccl needs one distinct GPU per rank");
+      c.transport = "nccl";
+    } else {
+      fail(errc::invalid_argument, "EINPLAN_TRANSPORT: \"nccl\" or \"peer\"");
+    }
+  }
+  return c;
+}
+
+using gpu::cuda_ok;
+
+// The tail of run() on the rank that holds the gathered output.
+void finish_report(gpu::ScheduleExecutor& ex, const std::vector<const double*>& globals,
+                   const RunOptions& opts, SimulationReport& rep) {
+  rep.comm = ex.comm();
+  if (opts.corrupt_output && !rep.output.data.empty()) rep.output.data[0] += 1.0;
+  if (opts.verify) ex.verify(globals, rep.output.data.data(), opts.tolerance, rep);
+}
+
+// One host thread per GPU (rank r on device dev[r]); every thread owns its
+// rank's blocks, the collectives run over NCCL or peer memory.
+void run_threads(const Pipeline& pipe, const std::vector<const double*>& globals,
+                 const RunOptions& opts, const ExecChoice& ch, SimulationReport& rep) {
+  const int procs = static_cast<int>(pipe.schedule.procs);
+  std::shared_ptr<gpu::PeerShared> shared;
+  std::vector<void*> comms(static_cast<std::size_t>(procs), nullptr);
+  if (ch.transport == "peer") {
+    shared = gpu::PeerShared::for_threads(procs);
+  } else {
+#ifdef EB_HAVE_NCCL
+    std::vector<ncclComm_t> c(static_cast<std::size_t>(procs));
+    const ncclResult_t r = ncclCommInitAll(c.data(), procs, ch.dev.data());
+    if (r != ncclSuccess)
+      throw eb::DeviceError(std::string("ncclCommInitAll: ") + ncclGetErrorString(r));
+    for (int k = 0; k < procs; ++k) comms[static_cast<std::size_t>(k)] = c[static_cast<std::size_t>(k)];
+#endif
+  }
+  std::vector<std::exception_ptr> errs(static_cast<std::size_t>(procs));
+  std::vector<std::string> msgs(static_cast<std::size_t>(procs));
+  auto body = [&](int r) {
+    std::unique_ptr<gpu::Transport> tp;
+    try {
+      cuda_ok(cudaSetDevice(ch.dev[static_cast<std::size_t>(r)]), "cudaSetDevice");
+      if (shared) {
+        tp = std::make_unique<gpu::PeerTransport>(std::make_shared<gpu::PeerComm>(shared, r), procs);
+      } else {
+#ifdef EB_HAVE_NCCL
+        tp = std::make_unique<gpu::NcclTransport>(comms[static_cast<std::size_t>(r)], procs, r);
+        comms[static_cast<std::size_t>(r)] = nullptr;  // owned by the transport now
+#endif
+      }
+      cudaStream_t st = nullptr;
+      cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+      {
+        gpu::ScheduleExecutor ex(pipe, tp.get(), st);
+        ex.stage_inputs(globals);
+        ex.execute();
+        if (r == 0) {
+          rep.output = DenseTensor(pipe.spec.shape_of(pipe.spec.output));
+          ex.gather(rep.output.data.data());
+          finish_report(ex, globals, opts, rep);
+        } else {
+          ex.gather(nullptr);
+        }
+      }
+      cudaStreamDestroy(st);
+    } catch (const std::exception& e) {
+      errs[static_cast<std::size_t>(r)] = std::current_exception();
+      msgs[static_cast<std::size_t>(r)] = e.what();
+      if (shared) shared->abort();
+    } catch (...) {
+      errs[static_cast<std::size_t>(r)] = std::current_exception();
+      if (shared) shared->abort();
+    }
+  };
+  int prev = 0;
+  cudaGetDevice(&prev);
+  std::vector<std::thread> th;
+  for (int r = 0; r < procs; ++r) th.emplace_back(body, r);
+  for (auto& t : th) t.join();
+  cudaSetDevice(prev);
+#ifdef EB_HAVE_NCCL
+  for (void* c : comms)
+    if (c) ncclCommDestroy(static_cast<ncclComm_t>(c));
+#endif
+  // report the failing rank's own error, not a peer's "another rank failed"
+  std::exception_ptr first;
+  for (int r = 0; r < procs; ++r) {
+    const auto& e = errs[static_cast<std::size_t>(r)];
+    if (!e) continue;
+    if (!first) first = e;
+    if (msgs[static_cast<std::size_t>(r)].find("another rank failed") == std::string::npos) {
+      first = e;
+      break;
+    }
+  }
+  if (first) std::rethrow_exception(first);
+  rep.exec_mode = "devices";
+  rep.devices = ch.dev;
+  rep.transport = ch.transport;
+}
+
+}  // namespace
+
+// The reference's C++ entry point (executor.cpp:156-263) on the GPUs: one
+// host thread per GPU when procs fits the visible devices, else every
+// virtual rank on the current device (choose_execution).
 SimulationReport run(const Schedule& schedule, const EinsumSpec& spec, const ContractionTree& tree,
                      const std::vector<DenseTensor>& inputs, const RunOptions& opts) {
   if (inputs.size() != static_cast<std::size_t>(tree.n_inputs))
@@ -1056,20 +1502,28 @@ SimulationReport run(const Schedule& schedule, const EinsumSpec& spec, const Con
   pipe.spec = spec;
   pipe.tree = tree;
   pipe.schedule = schedule;
+  std::vector<const double*> globals;
+  for (const auto& t : inputs) globals.push_back(t.data.data());
+  SimulationReport rep;
+  rep.seed = opts.seed;
+  const ExecChoice ch = choose_execution(schedule.procs);
+  if (ch.threads) {
+    run_threads(pipe, globals, opts, ch, rep);
+    return rep;
+  }
   gpu::VirtualTransport vt(schedule.procs);
   cudaStream_t st = nullptr;
   gpu::ScheduleExecutor ex(pipe, &vt, st);
-  std::vector<const double*> globals;
-  for (const auto& t : inputs) globals.push_back(t.data.data());
   ex.stage_inputs(globals);
   ex.execute();
-  SimulationReport rep;
-  rep.seed = opts.seed;
   rep.output = DenseTensor(spec.shape_of(spec.output));
   ex.gather(rep.output.data.data());
-  rep.comm = ex.comm();
-  if (opts.corrupt_output && !rep.output.data.empty()) rep.output.data[0] += 1.0;
-  if (opts.verify) ex.verify(globals, rep.output.data.data(), opts.tolerance, rep);
+  finish_report(ex, globals, opts, rep);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  rep.exec_mode = "virtual";
+  rep.devices = {dev};
+  rep.transport = "virtual";
   return rep;
 }
 

@@ -6,12 +6,14 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <memory>
 #include <set>
 #include <string>
 #include <vector>
 
 #include "einplan_b200.h"
 #include "einplan_host.hpp"
+#include "peer.hpp"
 
 namespace einplan {
 namespace gpu {
@@ -39,20 +41,38 @@ class DeviceArena {
   std::vector<void*> live_;
 };
 
-// How ranks exchange data: all virtual ranks on one device, or one rank per
-// process over NCCL.
+// How ranks exchange data: all virtual ranks on one device; one rank per
+// process (or host thread) over NCCL; or one rank per process / thread over
+// peer memory (PeerTransport: CUDA IPC or P2P pointers plus a host barrier).
+// Executors built `like=` another share its transport, and with it one
+// communication stream: every rank then issues its collectives in the same
+// order on one stream (NCCL's rule for operations on several communicators).
 class Transport {
  public:
-  virtual ~Transport() = default;
+  virtual ~Transport();
   virtual bool owns(std::int64_t rank) const = 0;
   virtual bool is_virtual() const = 0;
+  // blocks of non-owned ranks are peer-mapped device pointers (PeerTransport)
+  virtual bool peer_mapped() const { return false; }
   virtual std::int64_t allreduce(const TensorPlacement& place, const ReductionGroup& grp,
                                  std::vector<DevBlock>& blocks,
                                  std::vector<std::int64_t>& per_rank_sent, cudaStream_t st) = 0;
   virtual void redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
                             std::vector<DevBlock>& dst, cudaStream_t st) = 0;
+  // make the canonical output blocks readable by rank 0 (collective)
   virtual void gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
                               cudaStream_t st) = 0;
+  // after rank 0 copied them out: release staging (collective)
+  virtual void gather_done(std::vector<DevBlock>& blocks, cudaStream_t st) {
+    (void)blocks;
+    (void)st;
+  }
+  // the process's communication stream (created on first use, on the
+  // current device)
+  cudaStream_t comm_stream();
+
+ private:
+  cudaStream_t comm_stream_ = nullptr;
 };
 
 class VirtualTransport final : public Transport {
@@ -71,10 +91,43 @@ class VirtualTransport final : public Transport {
   std::int64_t procs_;
 };
 
+// One rank per process or host thread; every rank's exchanged blocks live in
+// its executor's exchange heap, mapped by every peer (peer.hpp).
+//   allreduce: each member sums the group's partials in ascending rank order
+//     from 0.0 straight out of the peers' heaps (executor.cpp:91-98), then
+//     writes the sum over its own partial once every member has read it;
+//   redistribute: each destination pulls its boxes from the canonical
+//     source's heap with strided box copies (redistribute.cpp:185-206) —
+//     no pack, no unpack, one pass over the link;
+//   gather: rank 0 reads the canonical blocks from the peers' heaps.
+class PeerTransport final : public Transport {
+ public:
+  PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks);
+  bool owns(std::int64_t r) const override { return r == comm_->rank(); }
+  bool is_virtual() const override { return false; }
+  bool peer_mapped() const override { return true; }
+  std::int64_t allreduce(const TensorPlacement& place, const ReductionGroup& grp,
+                         std::vector<DevBlock>& blocks, std::vector<std::int64_t>& per_rank_sent,
+                         cudaStream_t st) override;
+  void redistribute(const RedistributionPlan& plan, const std::vector<DevBlock>& src,
+                    std::vector<DevBlock>& dst, cudaStream_t st) override;
+  void gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
+                      cudaStream_t st) override;
+  void gather_done(std::vector<DevBlock>& blocks, cudaStream_t st) override;
+  PeerComm& comm() { return *comm_; }
+
+ private:
+  std::shared_ptr<PeerComm> comm_;
+  std::int64_t nranks_;
+};
+
 #ifdef EB_HAVE_NCCL
 class NcclTransport final : public Transport {
  public:
+  // one process per GPU: communicator from a 128-byte ncclUniqueId
   NcclTransport(const void* unique_id, std::int64_t nranks, std::int64_t rank);
+  // one host thread per GPU: a communicator of ncclCommInitAll (owned)
+  NcclTransport(void* comm, std::int64_t nranks, std::int64_t rank);
   ~NcclTransport() override;
   bool owns(std::int64_t r) const override { return r == rank_; }
   bool is_virtual() const override { return false; }
@@ -85,12 +138,20 @@ class NcclTransport final : public Transport {
                     std::vector<DevBlock>& dst, cudaStream_t st) override;
   void gather_to_root(const TensorPlacement& place, std::vector<DevBlock>& blocks,
                       cudaStream_t st) override;
+  void gather_done(std::vector<DevBlock>& blocks, cudaStream_t st) override;
 
  private:
+  // packing buffer for the messages of one redistribution, reused across
+  // runs (grown on demand; stream-ordered)
+  double* staging(std::int64_t elems, cudaStream_t st);
+
   std::int64_t rank_, nranks_;
   void* world_ = nullptr;
   std::map<std::string, void*> split_;
-  DeviceArena arena_;
+  double* staging_ = nullptr;
+  std::int64_t staging_elems_ = 0;
+  cudaEvent_t staging_done_ = nullptr;  // last use of staging_ (any stream)
+  std::vector<double*> gathered_;  // rank 0: receive buffers of one gather
 };
 #endif
 
@@ -106,6 +167,12 @@ class ScheduleExecutor {
   // process needs the global tensor (e.g. C5's 69 GB X at P = 8).
   void local_block(int k, std::vector<std::int64_t>& base, std::vector<std::int64_t>& shape) const;
   void stage_block(int k, const double* host_block);
+  // Virtual ranks without the global tensor: stage operand k from a host
+  // buffer holding the global sub-box [base, base + shape) of it; every owned
+  // rank's block lying inside the region is copied (returns how many).  E.g.
+  // C5 at P = 8 on one GPU, one 8.6 GB i-slab at a time instead of 69 GB.
+  int stage_region(int k, const std::vector<std::int64_t>& base,
+                   const std::vector<std::int64_t>& shape, const double* host);
   // Use another executor's staged device blocks for operand k (same tensor,
   // same placement on every owned rank): e.g. one X for the three MTTKRP
   // modes of a CP-ALS sweep.
@@ -133,6 +200,7 @@ class ScheduleExecutor {
   const CommStats& comm() const { return comm_; }
   const Pipeline& pipeline() const { return pipe_; }
   std::vector<std::int64_t> output_shape() const;
+  Transport* transport() const { return transport_; }
   int launches_fused() const { return launches_fused_; }
   int launches_ttm() const { return launches_ttm_; }
   int launches_generic() const { return launches_generic_; }
@@ -145,7 +213,15 @@ class ScheduleExecutor {
                       const DevBlock& b);
   const RedistRecord* find_redist(int to_term, const std::string& t) const;
   void* workspace(std::size_t bytes);
-  DevBlock new_block(const TermPlan& term, const std::string& idx, std::int64_t rank, bool zero);
+  // is_output: the term's output block — placed in the exchange heap when
+  // the transport maps peers' blocks and the tensor leaves the rank
+  DevBlock new_block(const TermPlan& term, const std::string& idx, std::int64_t rank, bool zero,
+                     bool is_output = false);
+  // Exchange heap (PeerTransport): one slot per term output that is reduced,
+  // redistributed or gathered, sized for the largest rank's block so every
+  // rank computes the same offsets; (re)allocated collectively.
+  void prepare_heap();
+  void map_peer_blocks(const TermPlan& term, std::vector<DevBlock>& blocks);
   bool try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
                         const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
   // Two chained TTM steps of one term on the fused eb_ttm2 kernel.
@@ -170,13 +246,12 @@ class ScheduleExecutor {
   CommStats comm_;
   int launches_fused_ = 0, launches_ttm_ = 0, launches_generic_ = 0;
   bool async_reduce_ = false, comm_pending_ = false;
-  cudaStream_t comm_stream_ = nullptr;
   cudaEvent_t ev_compute_ = nullptr, ev_comm_ = nullptr;
-  // EB_FUSE_TTM2=0 runs TTM-pair terms as two eb_contract launches (A/B checks)
-  bool fuse_ttm_ = [] {
-    const char* v = std::getenv("EB_FUSE_TTM2");
-    return !(v && v[0] == '0');
-  }();
+  // exchange heap (PeerTransport only)
+  char* heap_ = nullptr;
+  std::size_t heap_bytes_ = 0;
+  std::vector<char*> heap_peers_;
+  std::map<int, std::size_t> heap_slot_;  // term index -> byte offset
 };
 
 }  // namespace gpu

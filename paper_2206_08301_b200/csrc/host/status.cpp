@@ -14,7 +14,11 @@ const char* error_cstr() { return g_error.c_str(); }
 extern "C" const char* eb_last_error(void) { return eb::error_cstr(); }
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <set>
 #include <utility>
 #include <vector>
 
@@ -25,8 +29,37 @@ std::atomic<long long> g_launches{0};
 std::atomic<bool> g_timing{false};
 std::mutex g_mu;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
-cudaEvent_t g_open = nullptr;
+thread_local cudaEvent_t g_open = nullptr;  // one open bracket per launching thread
+
+Options read_env() {
+  Options o;
+  auto flag = [](const char* n) {
+    const char* v = std::getenv(n);
+    return v && v[0] && v[0] != '0';
+  };
+  o.no_fused_tma = flag("EB_NO_FUSED_TMA");
+  o.no_rf = flag("EB_NO_RF");
+  if (const char* v = std::getenv("EB_RF_CFG")) std::sscanf(v, "%dx%d", &o.rf_rt, &o.rf_os);
+  if (const char* v = std::getenv("EB_TTM2_VARIANT")) o.ttm2_variant = std::atoi(v);
+  if (const char* v = std::getenv("EB_FUSE_TTM2")) o.fuse_ttm2 = v[0] != '0';
+  return o;
+}
+
+Options g_opts = read_env();  // at library load
+std::mutex g_attr_mu;
+std::set<std::pair<const void*, int>> g_attr_done;
 }  // namespace
+
+const Options& options() { return g_opts; }
+
+void set_smem_attr_once(const void* kernel, int bytes) {
+  int dev = 0;
+  EB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.count({kernel, dev})) return;
+  EB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_attr_done.insert({kernel, dev});
+}
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -51,6 +84,34 @@ void main_kernel_end(cudaStream_t st) {
 }  // namespace eb
 
 extern "C" long long eb_launch_count(void) { return eb::g_launches.load(); }
+
+// Options (status.hpp): not thread-safe against concurrent launches; set
+// them between runs.
+extern "C" int eb_set_option(const char* name, const char* value) {
+  return eb::guard([&] {
+    if (!name || !value) throw eb::InvalidError("eb_set_option: null argument");
+    eb::Options& o = eb::g_opts;
+    const int v = std::atoi(value);
+    if (!std::strcmp(name, "no_fused_tma")) {
+      o.no_fused_tma = v != 0;
+    } else if (!std::strcmp(name, "no_rf")) {
+      o.no_rf = v != 0;
+    } else if (!std::strcmp(name, "rf_cfg")) {
+      int rt = 0, os = 0;
+      if (value[0] && std::strcmp(value, "auto") && std::sscanf(value, "%dx%d", &rt, &os) != 2)
+        throw eb::InvalidError("eb_set_option: rf_cfg is \"RTxOS\" or \"auto\"");
+      o.rf_rt = rt;
+      o.rf_os = os;
+    } else if (!std::strcmp(name, "ttm2_variant")) {
+      if (v < 0 || v > 2) throw eb::InvalidError("eb_set_option: ttm2_variant is 0, 1 or 2");
+      o.ttm2_variant = v;
+    } else if (!std::strcmp(name, "fuse_ttm2")) {
+      o.fuse_ttm2 = v != 0;
+    } else {
+      throw eb::InvalidError(std::string("eb_set_option: unknown option \"") + name + "\"");
+    }
+  });
+}
 
 extern "C" void eb_timer_enable(int on) { eb::g_timing.store(on != 0); }
 

@@ -56,4 +56,25 @@ namespace eb {
 void count_launch();
 void main_kernel_begin(cudaStream_t st);
 void main_kernel_end(cudaStream_t st);
+
+// Path-selection options.  Read ONCE from the environment when the library
+// loads (EB_NO_FUSED_TMA, EB_NO_RF, EB_RF_CFG, EB_TTM2_VARIANT, EB_FUSE_TTM2)
+// and changeable afterwards only through eb_set_option — no getenv on the
+// launch path.  Defaults are the shipped kernels; the others exist for the
+// parity tests of every path and for A/B measurements.
+struct Options {
+  int no_fused_tma = 0;   // per-16-column TMA boxes instead of one box per stage
+  int no_rf = 0;          // general contraction kernel instead of the resident-factor one
+  int rf_rt = 0, rf_os = 0;  // resident-factor tiling override (0 = automatic)
+  int ttm2_variant = 0;   // 0 auto, 1 / 2 = ttm2_ws_kernel<1> / <2>
+  int fuse_ttm2 = 1;      // executor: TTM pairs on eb_ttm2 (0: two eb_contract launches)
+};
+const Options& options();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).
+void set_smem_attr_once(const void* kernel, int bytes);
+template <typename K>
+inline void set_smem_once(K* kernel, int bytes) {
+  set_smem_attr_once(reinterpret_cast<const void*>(kernel), bytes);
+}
 }  // namespace eb

@@ -1017,11 +1017,7 @@ void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams
               cudaStream_t st) {
   using T = Tile<COL, NWM * WM, NT, KD, OS>;
   auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR, WS>;
-  static bool attr = false;
-  if (!attr) {
-    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem));
-    attr = true;
-  }
+  set_smem_once(kern, T::kSmem);
   main_kernel_begin(st);
   launch_pdl(kern, dim3(prm.G), dim3(WS ? 384 : (NWM * KS * OS + 1) * 32), T::kSmem, st, xm, um,
              prm);
@@ -1102,7 +1098,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   // padded); ROW stages Uᵀ per 64-column chunk.
   const int64_t pitch = (d->R + 15) / 16 * 16;
   // one box per operand per stage when the contiguous extent tiles by 16
-  prm.fused_tma = (p.col ? d->M % 16 == 0 : d->L % 16 == 0) && !std::getenv("EB_NO_FUSED_TMA") ? 1 : 0;
+  prm.fused_tma = (p.col ? d->M % 16 == 0 : d->L % 16 == 0) && !options().no_fused_tma ? 1 : 0;
   CUtensorMap umap_col;
   if (p.col) {
     const int64_t n = d->Q * pitch;
@@ -1258,7 +1254,7 @@ void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, doub
   EB_CUDA(cudaGetLastError());
   count_launch();
   CUtensorMap umap, xmap;
-  prm.fused_tma = d->L % 16 == 0 && !std::getenv("EB_NO_FUSED_TMA") ? 1 : 0;
+  prm.fused_tma = d->L % 16 == 0 && !options().no_fused_tma ? 1 : 0;
   if (prm.fused_tma) {
     const uint64_t udims[3] = {16, (uint64_t)d->R, (uint64_t)(d->L / 16)};
     const uint64_t ustr[2] = {(uint64_t)lp * 8, 128};

@@ -87,37 +87,59 @@ __global__ void group_sum_kernel(const GroupParams g) {
   }
 }
 
+struct GroupIntoParams {
+  const double* members[64];
+  int n;
+  int64_t len;
+  double* dst;
+};
+
+// acc = 0.0, then + member 0, member 1, ... (ascending rank): bitwise the
+// same sum as group_sum_kernel and the reference loop.
+__global__ void group_sum_into_kernel(const GroupIntoParams g) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int m = 0; m < g.n; ++m) acc += g.members[m][i];
+    g.dst[i] = acc;
+  }
+}
+
 constexpr int kMaxDim = 16;
+// A box copy after dim normalisation (unit dims dropped, dims that are
+// contiguous in both blocks merged): rows of `run` elements, outer dims
+// walked by a mixed-radix row index.
 struct BoxParams {
-  int nd;
+  int nd;             // outer dims (the run dim excluded)
   int64_t len[kMaxDim];
   int64_t sstride[kMaxDim], dstride[kMaxDim];
-  int64_t soff, doff;
-  int64_t total;
+  int64_t run;        // elements per row (in V units inside the kernel)
+  int64_t rows;
   const double* src;
   double* dst;
 };
 
-// threadIdx.x / blockIdx.x walk the innermost (contiguous) run of the box,
-// blockIdx.y (grid-stride) the outer rows: one row decomposition per block
-// row instead of per element.
-__global__ void copy_box_kernel(const BoxParams b) {
-  const int nd = b.nd;
-  const int64_t run = nd > 0 ? b.len[nd - 1] : 1;
-  const int64_t rows = b.total / (run > 0 ? run : 1);
-  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
-    int64_t r = row, so = b.soff, dof = b.doff;
-    for (int d = nd - 2; d >= 0; --d) {
+// TPR threads per row (a power of two <= blockDim), blockDim / TPR rows per
+// block; V = double2 when the run and every row start are 16-byte aligned.
+// Short rows (C4's t0 boxes: 16 doubles) no longer leave most of a
+// 256-thread block idle.
+template <typename V>
+__global__ void copy_box_kernel(const BoxParams b, int tpr) {
+  const int rpb = blockDim.x / tpr;
+  const int lane = threadIdx.x % tpr;
+  const int64_t run_v = b.run;
+  for (int64_t row = (int64_t)blockIdx.x * rpb + threadIdx.x / tpr; row < b.rows;
+       row += (int64_t)gridDim.x * rpb) {
+    int64_t r = row, so = 0, dof = 0;
+    for (int d = b.nd - 1; d >= 0; --d) {
       const int64_t c = r % b.len[d];
       r /= b.len[d];
       so += c * b.sstride[d];
       dof += c * b.dstride[d];
     }
-    const double* src = b.src + so;
-    double* dst = b.dst + dof;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < run;
-         i += (int64_t)gridDim.x * blockDim.x)
-      dst[i] = src[i];
+    const V* src = reinterpret_cast<const V*>(b.src + so);
+    V* dst = reinterpret_cast<V*>(b.dst + dof);
+    for (int64_t i = lane; i < run_v; i += tpr) dst[i] = src[i];
   }
 }
 
@@ -227,34 +249,103 @@ extern "C" int eb_group_sum(double* const* members, int n_members, int64_t n, vo
   });
 }
 
+extern "C" int eb_group_sum_into(const double* const* members, int n_members, int64_t n,
+                                 double* dst, void* stream) {
+  return eb::guard([&] {
+    if (n_members < 1 || n_members > 64) throw eb::InvalidError("eb_group_sum_into: 1..64 members");
+    if (!dst) throw eb::InvalidError("eb_group_sum_into: null destination");
+    eb::GroupIntoParams g;
+    std::memset(&g, 0, sizeof(g));
+    g.n = n_members;
+    g.len = n;
+    g.dst = dst;
+    for (int m = 0; m < n_members; ++m) g.members[m] = members[m];
+    if (n == 0) return;
+    eb::group_sum_into_kernel<<<eb::grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(g);
+    EB_CUDA(cudaGetLastError());
+    eb::count_launch();
+  });
+}
+
 extern "C" int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst,
                            const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
                            const int64_t* ox_lo, void* stream) {
   return eb::guard([&] {
     if (nd < 0 || nd > eb::kMaxDim) throw eb::InvalidError("eb_copy_box: bad rank");
+    // per-dim (len, src stride, dst stride), innermost last
+    int64_t len[eb::kMaxDim], ss[eb::kMaxDim], ds[eb::kMaxDim];
+    int64_t sstr = 1, dstr = 1, soff = 0, doff = 0;
+    for (int d = nd - 1; d >= 0; --d) {
+      len[d] = oy_hi[d] - oy_lo[d];
+      if (len[d] <= 0) return;
+      ss[d] = sstr;
+      ds[d] = dstr;
+      soff += oy_lo[d] * sstr;
+      doff += ox_lo[d] * dstr;
+      sstr *= src_shape[d];
+      dstr *= dst_shape[d];
+    }
+    // normalise: drop unit dims, merge a dim into the one inside it when
+    // both blocks store them contiguously
+    int64_t nl[eb::kMaxDim + 1], ns[eb::kMaxDim + 1], nds[eb::kMaxDim + 1];
+    int m = 0;
+    for (int d = 0; d < nd; ++d) {
+      if (len[d] == 1) continue;
+      nl[m] = len[d];
+      ns[m] = ss[d];
+      nds[m] = ds[d];
+      ++m;
+    }
+    if (m == 0) {
+      nl[0] = 1;
+      ns[0] = 1;
+      nds[0] = 1;
+      m = 1;
+    }
+    int w = m - 1;  // merge from the inside out
+    for (int d = m - 2; d >= 0; --d) {
+      if (ns[d] == nl[w] * ns[w] && nds[d] == nl[w] * nds[w]) {
+        nl[w] *= nl[d];
+        continue;
+      }
+      --w;
+      nl[w] = nl[d];
+      ns[w] = ns[d];
+      nds[w] = nds[d];
+    }
+    const int first = w;  // dims [first, m) remain
     eb::BoxParams b;
     std::memset(&b, 0, sizeof(b));
-    b.nd = nd;
-    b.src = src;
-    b.dst = dst;
-    int64_t ss = 1, ds = 1;
-    b.total = 1;
-    for (int d = nd - 1; d >= 0; --d) {
-      b.len[d] = oy_hi[d] - oy_lo[d];
-      if (b.len[d] <= 0) return;
-      b.sstride[d] = ss;
-      b.dstride[d] = ds;
-      b.soff += oy_lo[d] * ss;
-      b.doff += ox_lo[d] * ds;
-      ss *= src_shape[d];
-      ds *= dst_shape[d];
-      b.total *= b.len[d];
+    const int inner = m - 1;
+    // a strided innermost dim (never for row-major blocks) becomes rows of one element
+    const bool unit = ns[inner] == 1 && nds[inner] == 1;
+    const int64_t run = unit ? nl[inner] : 1;
+    const int outer_end = unit ? m - 1 : m;
+    b.nd = outer_end - first;
+    b.rows = 1;
+    for (int d = first; d < outer_end; ++d) {
+      b.len[d - first] = nl[d];
+      b.sstride[d - first] = ns[d];
+      b.dstride[d - first] = nds[d];
+      b.rows *= nl[d];
     }
-    const int64_t run = nd > 0 ? b.len[nd - 1] : 1;
-    const int64_t rows = b.total / run;
-    dim3 grid((unsigned)std::min<int64_t>((run + 255) / 256, 64),
-              (unsigned)std::min<int64_t>(rows, 65535));
-    eb::copy_box_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    const double* sp = src + soff;
+    double* dp = dst + doff;
+    bool vec = run % 2 == 0 && (reinterpret_cast<uintptr_t>(sp) % 16) == 0 &&
+               (reinterpret_cast<uintptr_t>(dp) % 16) == 0;
+    for (int d = 0; vec && d < b.nd; ++d) vec = b.sstride[d] % 2 == 0 && b.dstride[d] % 2 == 0;
+    b.src = sp;
+    b.dst = dp;
+    b.run = vec ? run / 2 : run;
+    int tpr = 1;
+    while (tpr < b.run && tpr < 256) tpr *= 2;
+    const int rpb = 256 / tpr;
+    const int64_t blocks = std::min<int64_t>((b.rows + rpb - 1) / rpb, 148 * 16);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (vec)
+      eb::copy_box_kernel<double2><<<(unsigned)blocks, 256, 0, st>>>(b, tpr);
+    else
+      eb::copy_box_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(b, tpr);
     EB_CUDA(cudaGetLastError());
     eb::count_launch();
   });

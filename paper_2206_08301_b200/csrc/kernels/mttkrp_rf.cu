@@ -437,7 +437,7 @@ struct RfPlan {
 };
 
 bool rf_plan(const eb_contract_desc* d, RfPlan& p) {
-  if (!d || d->variant != EB_ROW || d->mode != EB_REDUCE || std::getenv("EB_NO_RF")) return false;
+  if (!d || d->variant != EB_ROW || d->mode != EB_REDUCE || options().no_rf) return false;
   if (!d->X || !d->U || !d->out || d->P < 1 || d->M < 1 || d->Q < 1 || d->R < 1) return false;
   if (d->L < 16 || d->L > 64 || d->L % 16 || d->R > 24 || d->M >= 128) return false;
   if (d->n_pre < 0 || d->n_pre > kRfMaxFac || d->n_mid < 0 || d->n_mid > kRfMaxFac) return false;
@@ -448,13 +448,16 @@ bool rf_plan(const eb_contract_desc* d, RfPlan& p) {
   // one outer index of 64 rows when the mid extent is short
   p.rt = 16;
   p.os = 8;
-  if (const char* v = std::getenv("EB_RF_CFG")) {  // "RTxOS" (measurement knob)
-    int rt = 0, os = 0;
-    if (std::sscanf(v, "%dx%d", &rt, &os) == 2 && p.kb == 4 && p.nf == 3) {
-      p.rt = rt;
-      p.os = os;
-    }
+  if (options().rf_rt == 64 && options().rf_os == 1) {  // the short-mid tiling, forced (tests)
+    p.rt = 64;
+    p.os = 1;
   }
+#ifdef EB_AB_VARIANTS
+  if (options().rf_rt && p.kb == 4 && p.nf == 3) {  // measurement-only tilings (A/B builds)
+    p.rt = options().rf_rt;
+    p.os = options().rf_os;
+  }
+#endif
   if (d->Q < p.os) {
     p.rt = 64;
     p.os = 1;
@@ -493,11 +496,7 @@ template <int RT, int OS, int KB, int NF, bool PW = false>
 void rf_launch(const CUtensorMap& xm, const RfParams& prm, cudaStream_t st) {
   auto kern = mttkrp_rf_kernel<RT, OS, KB, NF, PW>;
   constexpr int smem = RfTile<RT, OS, KB>::kSmem;
-  static bool attr = false;
-  if (!attr) {
-    EB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  set_smem_once(kern, smem);
   main_kernel_begin(st);
   launch_pdl(kern, dim3(prm.G), dim3(PW ? 384 : 288), smem, st, xm, prm);
   main_kernel_end(st);
@@ -528,12 +527,14 @@ void rf_dispatch(int kb, int nf, const CUtensorMap& xm, const RfParams& prm, cud
 void rf_dispatch_cfg(const RfPlan& p, const CUtensorMap& xm, const RfParams& prm, cudaStream_t st) {
   if (p.rt == 16 && p.os == 8) return rf_dispatch<16, 8, true>(p.kb, p.nf, xm, prm, st);
   if (p.rt == 64 && p.os == 1) return rf_dispatch<64, 1>(p.kb, p.nf, xm, prm, st);
-  // measurement-only tilings (KB = 4, NF = 3)
+#ifdef EB_AB_VARIANTS
+  // measurement-only tilings (KB = 4, NF = 3), compiled into A/B builds only
   if (p.rt == 32 && p.os == 2) return rf_launch<32, 2, 4, 3>(xm, prm, st);
   if (p.rt == 32 && p.os == 4) return rf_launch<32, 4, 4, 3>(xm, prm, st);
   if (p.rt == 16 && p.os == 4) return rf_launch<16, 4, 4, 3>(xm, prm, st);
   if (p.rt == 8 && p.os == 8) return rf_launch<8, 8, 4, 3>(xm, prm, st);
   if (p.rt == 8 && p.os == 16) return rf_launch<8, 16, 4, 3>(xm, prm, st);
+#endif
   throw InvalidError("eb_contract: unsupported resident-factor tiling");
 }
 

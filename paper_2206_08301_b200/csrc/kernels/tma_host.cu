@@ -1,4 +1,5 @@
 // See tma_host.hpp.
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -55,12 +56,15 @@ CUtensorMap make_map(const void* ptr, int rank, const uint64_t* dims, const uint
   return m;
 }
 
-int sm_count() {
-  static int n = 0;
+int sm_count() {  // per device (one host thread per GPU may launch concurrently)
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  EB_CUDA(cudaGetDevice(&dev));
+  std::atomic<int>& slot = cache[dev & 63];
+  int n = slot.load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    EB_CUDA(cudaGetDevice(&dev));
     EB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    slot.store(n, std::memory_order_relaxed);
   }
   return n;
 }

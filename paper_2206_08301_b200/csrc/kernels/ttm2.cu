@@ -551,12 +551,7 @@ void validate(const eb_ttm2_desc* d) {
 
 template <int NW, bool PIPE>
 void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    EB_CUDA(cudaFuncSetAttribute(ttm2_kernel<NW, PIPE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NW>::Smem));
-    attr = true;
-  }
+  set_smem_once(ttm2_kernel<NW, PIPE>, Cfg<NW>::Smem);
   main_kernel_begin(st);
   launch_pdl(ttm2_kernel<NW, PIPE>, dim3(prm.G), dim3((NW + 1) * 32), Cfg<NW>::Smem, st, xmap, prm);
   main_kernel_end(st);
@@ -565,12 +560,7 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
 
 template <int JP>
 void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    EB_CUDA(cudaFuncSetAttribute(ttm2_ws_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 WsCfg<JP>::Smem));
-    attr = true;
-  }
+  set_smem_once(ttm2_ws_kernel<JP>, WsCfg<JP>::Smem);
   main_kernel_begin(st);
   launch_pdl(ttm2_ws_kernel<JP>, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), WsCfg<JP>::Smem, st,
              xmap, prm);
@@ -604,18 +594,24 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
                            (uint64_t)(d->Q1 * d->Q2 * d->M) * 8};
   const uint32_t box[4] = {16, (uint32_t)kJ, (uint32_t)kK, 1};
   const CUtensorMap xmap = make_map(d->X, 4, dims, str, box);
-  // tuning knobs (A/B measurements): consumer warps 8 / 16, step-1 pipelining
-  const char* v = std::getenv("EB_TTM2_WARPS");
-  const char* pp = std::getenv("EB_TTM2_PIPE");
-  // (measured, C5 terms at 1965 MHz: 8 warps unpipelined 1.56 ms, pipelined
-  // 1.60, 16 warps 1.73 / 2.19 — tools/ttm2_bench.py)
-  const bool pipe = pp && pp[0] == '1';
-  if (v && std::atoi(v) == 16)
-    pipe ? launch<16, true>(xmap, prm, st) : launch<16, false>(xmap, prm, st);
-  else if (v && std::atoi(v) == 8)
-    pipe ? launch<8, true>(xmap, prm, st) : launch<8, false>(xmap, prm, st);
-  else if (v && v[0] == 'w')
-    v[1] == '2' ? launch_ws<2>(xmap, prm, st) : launch_ws<1>(xmap, prm, st);
+#ifdef EB_AB_VARIANTS
+  // A/B builds only: the block-synchronous kernel with 8 / 16 consumer warps,
+  // step 1 optionally pipelined (measured, C5 terms at 1965 MHz: 8 warps
+  // unpipelined 1.56 ms, pipelined 1.60, 16 warps 1.73 / 2.19 —
+  // tools/ttm2_bench.py); EB_TTM2_AB = warps * 10 + pipe
+  if (const char* ab = std::getenv("EB_TTM2_AB")) {
+    const int v = std::atoi(ab);
+    if (v == 160) return launch<16, false>(xmap, prm, st);
+    if (v == 161) return launch<16, true>(xmap, prm, st);
+    if (v == 80) return launch<8, false>(xmap, prm, st);
+    if (v == 81) return launch<8, true>(xmap, prm, st);
+  }
+#endif
+  const int var = options().ttm2_variant;
+  if (var == 1)
+    launch_ws<1>(xmap, prm, st);
+  else if (var == 2)
+    launch_ws<2>(xmap, prm, st);
   else if (prm.items >= 16 * (int64_t)prm.G)  // long streams per CTA: C5 term 0 1.555 -> 1.484 ms
     launch_ws<1>(xmap, prm, st);
   else  // few items per CTA (C5 term 1: 0.105 vs 0.112 ms)

@@ -46,3 +46,21 @@ def ora():
     import oracle
     oracle.build(ref=True)
     return oracle
+
+
+_OPTION_DEFAULTS = {"no_fused_tma": 0, "no_rf": 0, "rf_cfg": "auto", "ttm2_variant": 0,
+                    "fuse_ttm2": 1}
+
+
+@pytest.fixture
+def opts(eb):
+    """Set kernel-path options (eb_set_option) for one test; restored after."""
+    touched = []
+
+    def set_(name, value):
+        touched.append(name)
+        eb.set_option(name, value)
+
+    yield set_
+    for n in touched:
+        eb.set_option(n, _OPTION_DEFAULTS[n])

@@ -68,11 +68,11 @@ SHAPES3 = [(40, 36, 50, 24), (130, 20, 34, 32), (64, 64, 64, 64), (20, 9, 18, 70
 @pytest.mark.parametrize("I,J,K,R", SHAPES3)
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("fused_tma", [True, False])
-def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, monkeypatch):
+def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, opts):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
     if not fused_tma:  # one TMA box per 16-wide block instead of one per operand
-        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
+        opts("no_fused_tma", 1)
     ext = dict(i=I, j=J, k=K, a=R)
     e = ["ijk,ja,ka->ia", "ijk,ia,ka->ja", "ijk,ia,ja->ka"][mode]
     ops = oracle.seeded_inputs(e, ext, 17 + mode)
@@ -95,11 +95,11 @@ def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, monkeypatch):
 @pytest.mark.parametrize("I,J,K,B", [(5, 40, 34, 64), (3, 70, 130, 16), (4, 33, 64, 24),
                                      (2, 9, 2, 100), (1, 256, 258, 8)])
 @pytest.mark.parametrize("fused_tma", [True, False])
-def test_contract_ttm(eb, I, J, K, B, fused_tma, monkeypatch):
+def test_contract_ttm(eb, I, J, K, B, fused_tma, opts):
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
     if not fused_tma:
-        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
+        opts("no_fused_tma", 1)
     ext = dict(i=I, j=J, k=K, b=B)
     e = "ijk,jb->ikb"
     X, U = oracle.seeded_inputs(e, ext, 13)
@@ -116,18 +116,15 @@ TTM2_SHAPES = [(2, 64, 64, 64, 16, 16), (3, 40, 7, 50, 16, 16), (1, 64, 9, 18, 5
 
 
 @pytest.mark.parametrize("P,Q1,Q2,M,N1,N2", TTM2_SHAPES)
-@pytest.mark.parametrize("knob", ["", "EB_TTM2_WARPS=w1", "EB_TTM2_WARPS=w2", "EB_TTM2_WARPS=8",
-                                  "EB_TTM2_WARPS=16", "EB_TTM2_WARPS=8,EB_TTM2_PIPE=1"])
-def test_ttm2_pair(eb, P, Q1, Q2, M, N1, N2, knob, monkeypatch):
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_ttm2_pair(eb, P, Q1, Q2, M, N1, N2, variant, opts):
     """eb_ttm2 = the two chained TTM steps pjkm,jb->pkmb ; pkmb,kc->pmbc of one
     term (TTMc-O5), ragged in every extent, against the oracle's n-ary loop —
-    the shipped warp-specialised kernels (JP = 1 / 2) and the measured
-    alternatives the EB_TTM2_* knobs select."""
+    the automatic choice and each shipped warp-specialised kernel (JP = 1 / 2)
+    forced with the ttm2_variant option."""
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
-    for kv in filter(None, knob.split(",")):
-        k, v = kv.split("=")
-        monkeypatch.setenv(k, v)
+    opts("ttm2_variant", variant)
     e = "pjkm,jb,kc->pmbc"
     ext = dict(p=P, j=Q1, k=Q2, m=M, b=N1, c=N2)
     ops = oracle.seeded_inputs(e, ext, 23)
@@ -161,7 +158,7 @@ def _ttmc_o5_chain(ext, ops):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
-def test_ttmc_o5_fused_terms(eb, P, monkeypatch):
+def test_ttmc_o5_fused_terms(eb, P, opts):
     """Both TTMc-O5 terms ([t0,t1], [t2,out]: the C5 partition at these
     extents, with the i2m2 / i2c2 / i2l2m2 / i2b2c2 grids of P=4, 8) run on
     eb_ttm2 — two fused launches per rank — and match the oracle chain and
@@ -179,7 +176,7 @@ def test_ttmc_o5_fused_terms(eb, P, monkeypatch):
     assert st["fused_launches"] == 2 * P and st["ttm_launches"] == 0, st
     assert st["generic_launches"] == 0, st
     check(ex.gather(), want)
-    monkeypatch.setenv("EB_FUSE_TTM2", "0")
+    opts("fuse_ttm2", 0)
     ex = eb.Executor(e, ext, P)
     ex.stage(ops)
     ex.run()
@@ -193,12 +190,12 @@ MTTKRP2_SHAPES = [(130, 20, 34, 32), (256, 64, 64, 24), (128, 9, 2, 8), (300, 40
 
 @pytest.mark.parametrize("I,J,K,R", MTTKRP2_SHAPES)
 @pytest.mark.parametrize("fused_tma", [True, False])
-def test_mttkrp2_dimension_tree_pair(eb, I, J, K, R, fused_tma, monkeypatch):
+def test_mttkrp2_dimension_tree_pair(eb, I, J, K, R, fused_tma, opts):
     """eb_mttkrp2: one pass over X gives the mode-0 and the mode-1 MTTKRP
     (T = X x_k C folded with B and with A), each equal to the oracle's own
     naive_evaluate of that mode's einsum."""
     if not fused_tma:
-        monkeypatch.setenv("EB_NO_FUSED_TMA", "1")
+        opts("no_fused_tma", 1)
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
     ext = dict(i=I, j=J, k=K, a=R)
@@ -346,13 +343,14 @@ def test_contract_order5_all_krp_rows(eb):
     check(got, want)
 
 
-@pytest.mark.parametrize("cfg", ["64x1", "32x2", "32x4", "16x4", "16x8", "8x8", "8x16"])
-def test_resident_factor_measurement_tilings(eb, cfg, monkeypatch):
-    """Every tiling the EB_RF_CFG measurement knob can select (the C3 term
-    shape, L = 64, R = 24) gives the oracle's result."""
+@pytest.mark.parametrize("cfg", ["64x1", "16x8"])
+def test_resident_factor_measurement_tilings(eb, cfg, opts):
+    """Both shipped resident-factor tilings (forced with the rf_cfg option)
+    on the C3 term shape (L = 64, R = 24) give the oracle's result.  (The
+    measurement-only tilings are compiled into EB_AB_VARIANTS builds only.)"""
     from paper_2206_08301_b200 import _capi as C
     torch = _torch()
-    monkeypatch.setenv("EB_RF_CFG", cfg)
+    opts("rf_cfg", cfg)
     e = "ijklm,ja,ka,la,ma->ia"
     ext = dict(i=64, j=4, k=4, l=8, m=64, a=24)
     ops = oracle.seeded_inputs(e, ext, 21)
@@ -451,8 +449,8 @@ RF_CASES = [  # (einsum, extents, P, M, Q, L, #pre, #mid): the resident-factor p
 
 
 @pytest.mark.parametrize("case", range(len(RF_CASES)))
-@pytest.mark.parametrize("knob", ["", "EB_RF_CFG=64x1", "EB_NO_RF=1"])
-def test_contract_resident_factor_path(eb, case, knob, monkeypatch):
+@pytest.mark.parametrize("knob", ["", "rf_cfg=64x1", "no_rf=1"])
+def test_contract_resident_factor_path(eb, case, knob, opts):
     """Short contracted mode (L <= 64, L % 16 == 0), R <= 24, M < 128: the
     resident-factor kernel (mttkrp_rf.cu; the paired 16 x 8 tiling, or the
     64 x 1 one) and, with EB_NO_RF, the general kernel — all against the
@@ -462,7 +460,7 @@ def test_contract_resident_factor_path(eb, case, knob, monkeypatch):
     e, ext, P, M, Q, L, npre, nmid = RF_CASES[case]
     if knob:
         k, v = knob.split("=")
-        monkeypatch.setenv(k, v)
+        opts(k, v)
     ops = oracle.seeded_inputs(e, ext, 31 + case)
     want = oracle.naive_evaluate(e, ext, ops)
     g = [torch.from_numpy(o).cuda() for o in ops]
@@ -823,6 +821,9 @@ def test_run_report_matches_reference_report(eb, name, einsum, ext, P):
     rst, theirs = oracle.ref_run_json(einsum, ext, P, 1024.0, seed=7, verify=True)
     assert st == rst == 0
     a, b = json.loads(mine), json.loads(theirs)
+    # the B200 extension field (how the ranks ran) comes after every reference field
+    assert list(a.keys())[-1] == "execution" and "execution" not in b
+    assert a.pop("execution")["mode"] in ("devices", "virtual")
     sa, sb = a["output"].pop("sum"), b["output"].pop("sum")
     assert abs(sa - sb) <= 1e-11 * max(1.0, abs(sb))
     ea = a["verification"].pop("max_rel_error")

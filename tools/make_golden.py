@@ -70,8 +70,42 @@ def outputs(which):
             print(tag, f"run() {secs:.1f}s", flush=True)
 
 
+def c5_slabs(slabs):
+    """C5 goldens for P = 2, 4, 8 (global X = random_tensor(
+    (64P, 64, 64, 64, 64), 0), one row-major stream).  Mode-0 TTMc rows
+    depend only on X[i], so output rows [64p, 64p + 64) of every P > p are the
+    reference run() at P = 1 on the 64-row slab p of the seed-0 stream (stream
+    elements [p*64^5, (p+1)*64^5)) with the same four 64x16 factors (seeds
+    1..4).  Slab 0 is the P = 1 golden (C5_summary.json)."""
+    meta_path = os.path.join(GOLD, "reference_runs.json")
+    meta = json.load(open(meta_path)) if os.path.exists(meta_path) else {}
+    c = CONFIGS["C5"]
+    e = c["einsums"][0]
+    ext = c["extents"](1)
+    ins, _ = oracle.parse(e)
+    n = 64 ** 5
+    for p in slabs:
+        tag = f"C5_slab{p}"
+        if os.path.exists(os.path.join(GOLD, f"{tag}_summary.json")):
+            continue
+        t = time.time()
+        ops = [oracle.random_tensor(oracle.shape_of(ins[0], ext), 0, skip=p * n)]
+        ops += [oracle.random_tensor(oracle.shape_of(s, ext), k + 1) for k, s in enumerate(ins[1:])]
+        out, secs, comm = oracle.ref_run(e, ext, 1, ops)
+        wall = time.time() - t
+        del ops
+        with open(os.path.join(GOLD, f"{tag}_summary.json"), "w") as f:
+            json.dump(summary(out), f)
+        meta[tag] = {"einsum": e, "extents": ext, "procs": 1, "x_stream_skip": p * n,
+                     "run_seconds": secs, "wall_seconds": wall, "comm": list(comm), "threads": 1}
+        json.dump(meta, open(meta_path, "w"), indent=1)
+        print(tag, f"run() {secs:.1f}s wall {wall:.1f}s", flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "plans":
         plans()
+    elif sys.argv[1] == "c5slabs":
+        c5_slabs([int(x) for x in sys.argv[2:]] or list(range(1, 8)))
     else:
         outputs(sys.argv[2:] or ["C1", "C3", "C5", "C2", "C4"])
