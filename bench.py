@@ -218,50 +218,113 @@ class ClockSampler:
 # ------------------------------------------------------- reference arm --
 
 # i-rows of X per reference run() in the CPU samples (a few seconds of
-# single-threaded reference work each); every config's output mode 0 (and
-# C2's sweep) is a sum over independent i-slabs, so a slab is a faithful,
-# proportionally smaller instance of the same computation
+# single-threaded reference work each).  Every config's mode-0 output (and
+# C2's sweep) is a sum over independent i-slabs of X, so a slab of the REAL
+# seed-0 tensor is an exact, proportionally smaller piece of the same
+# computation: mode-0 outputs are the slab's output rows, the C2 mode-1 /
+# mode-2 outputs are sums of the slabs' partial outputs.
 REF_SLAB_ROWS = {"C1": 16, "C2": 8, "C3": 1, "C4": 4, "C5": 1}
 
 
-def _ref_sample_step(threads: int, rows: int, config: str = "C2"):
-    """One bounded sample of `config` on the reference implementation:
-    `threads` concurrent reference run() calls (P=1), each on its own slab of
-    `rows` i-rows of X (C2: all three modes).  Returns (flops, seconds)."""
-    import oracle
-    from tests.configs import CONFIGS
-    c = CONFIGS[config]
-    work = []
-    flops_per_mode = {}
-    ext = dict(c["extents"](1))
-    ext["i"] = rows
-    for t in range(threads):
-        xin = c["einsums"][0].split("->")[0].split(",")[0]
-        X = oracle.random_tensor(oracle.shape_of(xin, ext), 100 + t)
-        per_mode = []
-        for mode, e in enumerate(c["einsums"]):
+class RefWorkload:
+    """The config's real inputs (seed-0 X, the config's factor seeds — the
+    same tensors the GPU arm stages) cut into i-slabs that successive reference
+    steps rotate through; the slab outputs are reassembled and, once every row
+    was covered, checked against the reference's own full-size goldens."""
+
+    def __init__(self, config: str):
+        import oracle
+        from tests.configs import CONFIGS
+        c = CONFIGS[config]
+        self.config = config
+        self.ext = dict(c["extents"](1))
+        self.einsums = c["einsums"]
+        xin = self.einsums[0].split("->")[0].split(",")[0]
+        self.I = self.ext["i"]
+        self.X = oracle.random_tensor(oracle.shape_of(xin, self.ext), 0)
+        self.factors = []  # per mode: full factor operands
+        self.flops_per_row = 0
+        for e in self.einsums:
             ins, _ = oracle.parse(e)
-            seeds = ({"i": 1, "j": 2, "k": 3} if config == "C2"
-                     else {s: k + 1 for k, s in enumerate(ins[1:])})
-            ops = [X] + [oracle.random_tensor(oracle.shape_of(s, ext),
-                                              seeds[s[0]] if config == "C2" else seeds[s])
-                         for s in ins[1:]]
-            per_mode.append((e, ext, ops))
-            if e not in flops_per_mode:
-                flops_per_mode[e] = json.loads(oracle.ref_plan_json(e, ext, 1))["tree"]["total_flops"]
-        work.append(per_mode)
-    flops = sum(flops_per_mode[e] for per_mode in work for e, _, _ in per_mode)
+            if config == "C2":
+                from tests.configs import C2_FACTOR_SEED
+                fs = [oracle.random_tensor(oracle.shape_of(t, self.ext), C2_FACTOR_SEED[t[0]])
+                      for t in ins[1:]]
+            else:
+                fs = [oracle.random_tensor(oracle.shape_of(t, self.ext), k + 1)
+                      for k, t in enumerate(ins[1:])]
+            self.factors.append(fs)
+            self.flops_per_row += json.loads(oracle.ref_plan_json(e, self.ext, 1))["tree"][
+                "total_flops"] / self.I
+        self.out = [None] * len(self.einsums)
+        self.covered = np.zeros(self.I, dtype=bool)
+
+    def slab_ops(self, mode, i0, rows):
+        """Operands of mode `mode` restricted to X[i0:i0+rows] (factors indexed
+        by i sliced alike)."""
+        import oracle
+        e = self.einsums[mode]
+        ins, _ = oracle.parse(e)
+        ops = [self.X[i0:i0 + rows]]
+        for t, f in zip(ins[1:], self.factors[mode]):
+            ops.append(np.ascontiguousarray(f[i0:i0 + rows]) if t[0] == "i" else f)
+        ext = dict(self.ext, i=rows)
+        return e, ext, ops
+
+    def absorb(self, mode, i0, rows, out):
+        e = self.einsums[mode]
+        full_shape = tuple(self.ext[c] for c in e.split("->")[1])
+        if self.out[mode] is None:
+            self.out[mode] = np.zeros(full_shape)
+        if e.split("->")[1][0] == "i":
+            self.out[mode][i0:i0 + rows] = out
+        else:  # C2 modes 1 / 2: the slab's partial sum
+            self.out[mode] += out
+        self.covered[i0:i0 + rows] = True
+
+    def check(self):
+        """Normwise error of the reassembled outputs against the reference's
+        goldens (None until every i-row has been covered)."""
+        if not self.covered.all():
+            return None
+        import oracle
+        errs = []
+        for mode, out in enumerate(self.out):
+            tag = f"C2_m{mode}" if self.config == "C2" else self.config
+            g = json.load(open(os.path.join(ROOT, "tests", "golden", f"{tag}_summary.json")))
+            idx = np.array(g["sample_index"])
+            errs.append(oracle.normwise_error(out.ravel()[idx], np.array(g["sample_value"])))
+        return max(errs)
+
+
+def _ref_sample_step(threads: int, rows: int, wl: "RefWorkload", step: int):
+    """One bounded sample of the config on the reference implementation:
+    `threads` concurrent reference run() calls (P = 1), each on the next slab
+    of `rows` i-rows of the real X (C2: all three modes); steps rotate over
+    the slabs.  Returns (flops, seconds)."""
+    import oracle
+    nslab = wl.I // rows
+    work = []
+    for t in range(threads):
+        i0 = ((step * threads + t) % nslab) * rows
+        work.append([(m, i0, wl.slab_ops(m, i0, rows)) for m in range(len(wl.einsums))])
+    flops = wl.flops_per_row * rows * threads
+    results = [[None] * len(wl.einsums) for _ in range(threads)]
 
     def body(t):
-        for e, ext, ops in work[t]:
-            oracle.ref_run(e, ext, 1, ops)
+        for m, i0, (e, ext, ops) in work[t]:
+            results[t][m] = oracle.ref_run(e, ext, 1, ops)[0]
     ths = [threading.Thread(target=body, args=(t,)) for t in range(threads)]
     t0 = time.perf_counter()
     for th in ths:
         th.start()
     for th in ths:
         th.join()
-    return flops, time.perf_counter() - t0
+    dt = time.perf_counter() - t0
+    for t in range(threads):
+        for m, i0, _ in work[t]:
+            wl.absorb(m, i0, rows, results[t][m])
+    return flops, dt
 
 
 def cpu_kind():
@@ -278,30 +341,41 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     threads = max(1, min(cores, 32))
     rows = REF_SLAB_ROWS[args.config]
+    wl = RefWorkload(args.config)
+    step = 0
     for _ in range(args.warmup):
-        _ref_sample_step(threads, rows, args.config)
+        _ref_sample_step(threads, rows, wl, step)
+        step += 1
     tot_f, tot_s = 0, 0.0
     for _ in range(args.steps):
-        f, s = _ref_sample_step(threads, rows, args.config)
+        f, s = _ref_sample_step(threads, rows, wl, step)
+        step += 1
         tot_f += f
         tot_s += s
+    err = wl.check()
     value = tot_f / tot_s / 1e9
     sample = (f"{args.config} sample per step: {threads} concurrent reference run() calls (P=1, "
-              f"single-threaded each, oracle/_ref built from the reference sources), each on an "
-              f"{rows}-row i-slab of X{' (all 3 modes)' if args.config == 'C2' else ''}; "
-              f"GFLOP/s = reference tree flops / wall time")
+              f"single-threaded each, oracle/_ref built from the reference sources), each on the "
+              f"next {rows}-row i-slab of the config's own seed-0 X"
+              f"{' (all 3 modes)' if args.config == 'C2' else ''}, slabs rotating over all "
+              f"{wl.I} rows; GFLOP/s = reference tree flops / wall time")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference random_tensor, mt19937_64 seed 0 / factor seeds 1,2,3)",
+        "data": "synthetic: the same seed-0 X and factor streams as the B200 arm "
+                "(reference random_tensor, mt19937_64)",
         "config": {"workload": workload_label(args.config), "sample_rows_per_thread": rows,
-                   "threads": threads},
+                   "threads": threads, "same_inputs_as_b200_arm": True,
+                   "rows_covered": int(wl.covered.sum()), "rows_total": wl.I},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads,
                          "kind": cpu_kind(), "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        # reassembled slab outputs vs the reference's full-size goldens (sampled
+        # elements, normwise); null if the timed steps did not cover every row
+        "reassembled_vs_golden": err,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -321,8 +395,8 @@ CPU_LEG_ROWS = {"C1": 64, "C2": 16, "C3": 1, "C4": 8, "C5": 1}
 
 
 def cpu_baseline_leg(config="C2"):
-    """Rank 0, N = 1: the reference (or the oracle port) on a bounded sample,
-    single-threaded as the reference is (README.md:149-150)."""
+    """Rank 0, N = 1: the reference (or the oracle port) on a bounded sample
+    of the same inputs, single-threaded as the reference is (README.md:149-150)."""
     import oracle
     if not oracle.ref_available():
         try:
@@ -331,12 +405,13 @@ def cpu_baseline_leg(config="C2"):
             pass
     if oracle.ref_available():
         rows = CPU_LEG_ROWS[config]
-        f, s = _ref_sample_step(1, rows, config)
+        wl = RefWorkload(config)
+        f, s = _ref_sample_step(1, rows, wl, 0)
         what = "sweep (3 modes)" if config == "C2" else "run"
         return {"value": f / s / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
-                "sample": f"{config} {what} on an X slab of {rows} i-rows, reference run() at "
-                          "P=1, one host thread (the reference is single-threaded); "
-                          f"{s:.1f} s of CPU work"}
+                "sample": f"{config} {what} on X[0:{rows}] of the config's own seed-0 X, "
+                          "reference run() at P=1, one host thread (the reference is "
+                          f"single-threaded); {s:.1f} s of CPU work"}
     # Port: the C restatement on a smaller slab.
     ext = dict(i=4, j=1024, k=1024, a=32)
     t0 = time.perf_counter()

@@ -24,10 +24,10 @@ import paper_2206_08301_b200 as eb  # noqa: E402
 
 CASES = {
     # MTTKRP mode 0: one term, reduction groups (allreduce)
-    "mttkrp_m0": ("ijk,ja,ka->ia", dict(i=64, j=60, k=48, a=16), 3),
+    "mttkrp_m0": ("ijk,ja,ka->ia", dict(i=64, j=64, k=64, a=16), 3),
     "mttkrp_m2": ("ijk,ia,ja->ka", dict(i=40, j=36, k=64, a=8), 4),
     # TTMc order 3: two terms, t0 redistributed between the term grids
-    "ttmc3": ("ijk,jb,kc->ibc", dict(i=32, j=48, k=40, b=8, c=6), 5),
+    "ttmc3": ("ijk,jb,kc->ibc", dict(i=96, j=96, k=96, b=24, c=24), 5),
     # TTMc order 5 (both terms on eb_ttm2)
     "ttmc5": ("ijklm,jb,kc,ld,me->ibcde",
               dict(i=32, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12), 6),
