@@ -183,7 +183,9 @@ int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fas
 
 /* Path options (read once from EB_* environment variables at load; this
  * call changes them between runs): "no_fused_tma" 0/1, "no_rf" 0/1,
- * "rf_cfg" "RTxOS"|"auto", "ttm2_variant" 0/1/2, "fuse_ttm2" 0/1. */
+ * "rf_cfg" "RTxOS"|"auto", "ttm2_variant" 0/1/2, "fuse_ttm2" 0/1,
+ * "gemm" 0 auto / 1 forced / 2 off (wide GEMM steps: one launch over
+ * (row tile, 64-column block) items instead of per-64-column split-K). */
 int eb_set_option(const char* name, const char* value);
 
 /* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------

@@ -42,6 +42,7 @@ Options read_env() {
   if (const char* v = std::getenv("EB_RF_CFG")) std::sscanf(v, "%dx%d", &o.rf_rt, &o.rf_os);
   if (const char* v = std::getenv("EB_TTM2_VARIANT")) o.ttm2_variant = std::atoi(v);
   if (const char* v = std::getenv("EB_FUSE_TTM2")) o.fuse_ttm2 = v[0] != '0';
+  if (const char* v = std::getenv("EB_GEMM")) o.gemm = std::atoi(v);
   return o;
 }
 
@@ -107,6 +108,9 @@ extern "C" int eb_set_option(const char* name, const char* value) {
       o.ttm2_variant = v;
     } else if (!std::strcmp(name, "fuse_ttm2")) {
       o.fuse_ttm2 = v != 0;
+    } else if (!std::strcmp(name, "gemm")) {
+      if (v < 0 || v > 2) throw eb::InvalidError("eb_set_option: gemm is 0, 1 or 2");
+      o.gemm = v;
     } else {
       throw eb::InvalidError(std::string("eb_set_option: unknown option \"") + name + "\"");
     }

@@ -405,10 +405,13 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
           const int k0 = (int)(kc * KD);
           const int64_t ob = o * OS;  // first outer index of the stage
           if (!COL) {
+            // ROW + BATCHED is the GEMM mode: P = Q = 1, the item's "outer
+            // index" o is its 64-column block of the output (Uᵀ rows o*NP..)
+            const int ucol = BATCHED ? (int)(o * NT * 8) : 0;
             // the producer shares an SMSP with DMMA-saturated warps and gets
             // few issue slots: (p, q) advance incrementally (Q % OS == 0),
             // no 64-bit division per stage
-            if (o != t_o) {
+            if (!BATCHED && o != t_o) {
               if (t_o >= 0 && o == t_o + 1) {
                 tq += OS;
                 if (tq >= prm.Q) {
@@ -425,14 +428,14 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
               // X dims {16, M, Q, L/16, P}: box {16, MT, OS, KD/16, 1} -> [b][OS][MT][16]
               tma_load_5d(xs, &xmap, fb, 0, (int)(mt * MT), (int)tq, k0 / 16, (int)tp);
               // Uᵀ dims {16, cols, L/16}: box {16, NP, KD/16} -> [b][NP][16]
-              tma_load_3d(us, &umap, fb, 0, 0, k0 / 16);
+              tma_load_3d(us, &umap, fb, 0, ucol, k0 / 16);
             } else {
               // X map dims {L, M, Q, P}: box {16, MT, OS, 1} -> smem [OS][MT][16]
 #pragma unroll
               for (int b = 0; b < KD / 16; ++b) {
                 tma_load_4d(xs + b * OS * MT * 128, &xmap, fb, k0 + 16 * b, (int)(mt * MT),
                             (int)tq, (int)tp);
-                tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, 0);
+                tma_load_2d(us + b * NT * 8 * 128, &umap, fb, k0 + 16 * b, ucol);
               }
             }
           } else if (prm.fused_tma) {
@@ -747,16 +750,19 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       }
     } else if (BATCHED) {
-      // out[p][m][col0 + n], guarded at the ragged row / column edges.
+      // COL: out[p][m][col0 + n]; ROW (GEMM mode): out[m][64 o + n];
+      // guarded at the ragged row / column edges.
+      const int cbase = COL ? prm.col0 : (int)(o * NT * 8);
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const int64_t row = mt * MT + wm * WM + i * 8 + g;
         if (row < prm.M) {
-          double* dst = prm.out + (o * prm.M + row) * prm.ldo + prm.col0;
+          double* dst = COL ? prm.out + (o * prm.M + row) * prm.ldo + prm.col0
+                            : prm.out + row * prm.ldo + cbase;
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const int c = j * 8 + 2 * l;
-            const int gc = prm.col0 + c;
+            const int gc = cbase + c;
             if (gc + 1 < prm.R && ((reinterpret_cast<uintptr_t>(dst + c) & 15) == 0)) {
               *reinterpret_cast<double2*>(dst + c) = make_double2(acc[i][j][0], acc[i][j][1]);
             } else {
@@ -876,14 +882,33 @@ __global__ void reduce_two_kernel(const double* __restrict__ slots, double* __re
 }
 
 // Uᵀ staging for the ROW variant (TMA needs k innermost): ut[n][l] = u[l][col0+n].
+// Uᵀ[n][k] = U[k][col0 + n] through a 32 x 32 shared-memory tile: reads
+// coalesced along n, writes coalesced along k (block 32 x 8, grid over
+// (n tiles, k tiles)).
 __global__ void transpose_factor_kernel(const double* __restrict__ u, int64_t ldu, int64_t L,
                                         int cols, int col0, double* __restrict__ ut, int64_t ldt) {
+  __shared__ double tile[32][33];
   grid_dep_wait();
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)cols * L) return;
-  const int n = (int)(idx / L);
-  const int64_t k = idx % L;
-  ut[n * ldt + k] = u[k * ldu + col0 + n];
+  const int64_t n0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int64_t k = k0 + ty + r, n = n0 + tx;
+    tile[ty + r][tx] = (k < L && n < cols) ? u[k * ldu + col0 + n] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 32; r += 8) {
+    const int64_t n = n0 + ty + r, k = k0 + tx;
+    if (n < cols && k < L) ut[n * ldt + k] = tile[tx][ty + r];
+  }
+}
+
+void launch_transpose(const double* u, int64_t ldu, int64_t L, int cols, int col0, double* ut,
+                      int64_t ldt, cudaStream_t st) {
+  const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((L + 31) / 32));
+  launch_pdl(transpose_factor_kernel, grid, dim3(32, 8), 0, st, u, ldu, L, cols, col0, ut, ldt);
+  count_launch();
 }
 
 // COL staging: copy into an even-pitched [Q][pitch] buffer (TMA strides are
@@ -927,6 +952,11 @@ struct Plan {
   // tiles): CTAs take whole row tiles (ranges aligned to tiles) and write
   // out[m][col0 + n] directly — no partial slots, no reduction kernel
   bool direct = false;
+  // GEMM mode (ROW, no Khatri-Rao factors, P = Q = 1, R > 64, M >= 128):
+  // items = (row tile, 64-column block), each CTA runs the whole K loop of an
+  // item and writes its output tile directly — one launch for all columns,
+  // Uᵀ staged once, no split-K partials (the 1MM/2MM/3MM chains)
+  bool gemm = false;
   size_t u_bytes = 0;  // staged factor buffer (per chunk)
   size_t ws_bytes = 0; // partial slots (per chunk)
 };
@@ -962,6 +992,24 @@ Plan plan_of(const eb_contract_desc* d) {
   //   BATCHED          : 8 row warps x 16 (N >= 32), else 4 x 32 (M >= 128) or
   //                      4 x 16, 32-deep
   const int64_t outer = p.col ? d->P : d->P * d->Q;
+  // (auto: only with a full wave of items; the gemm option forces it on / off)
+  p.gemm = !p.col && !p.batched && d->P == 1 && d->Q == 1 && d->n_pre == 0 && d->n_mid == 0 &&
+           d->R > 64 && rows >= 128 && d->L % 16 == 0 && !options().no_fused_tma &&
+           options().gemm != 2 &&
+           (options().gemm == 1 || cdiv(rows, 128) * cdiv(d->R, 64) >= (int64_t)sm_count());
+  if (p.gemm) {
+    p.nwm = 8; p.wm = 16; p.ks = 1; p.kd = 32; p.os = 1; p.nt = 8;
+    p.mt = 128;
+    p.kin = d->L;
+    p.O = p.chunks;
+    p.KC = cdiv(d->L, p.kd);
+    p.mtiles = cdiv(rows, p.mt);
+    p.items = p.mtiles * p.O;
+    p.G = (int)std::min<int64_t>(p.items, (int64_t)sm_count());
+    p.u_bytes = ((size_t)d->R * ((d->L + 1) / 2 * 2) * sizeof(double) + 255) / 256 * 256;
+    p.ws_bytes = 0;
+    return p;
+  }
   if (p.batched) {
     // wide N (compute-bound TTM): 8 warps x 16 rows, two warps per SMSP
     // (C4 step 0: 92 % vs 80 % of peak); narrow N (HBM-bound): 4 x 32.
@@ -1060,6 +1108,7 @@ void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtenso
 
 void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                     const ContractParams& prm, cudaStream_t st) {
+  if (p.gemm) return launch_t<false, true, 8, 16, 1, 32, 1, 8>(xm, um, prm, st);
   if (p.batched) {
     if (p.nwm == 8) return dispatch_nt<true, true, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
     if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
@@ -1144,6 +1193,20 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     xmap = make_map(d->X, 3, dims, str, box);
   }
 
+  if (p.gemm) {  // Uᵀ [R][lp] once; one launch over (row tile, column block) items
+    const int64_t lp = (d->L + 1) / 2 * 2;
+    launch_transpose(d->U, ldu, d->L, (int)d->R, 0, ubuf, lp, st);
+    const uint64_t dims[3] = {16, (uint64_t)d->R, (uint64_t)(d->L / 16)};
+    const uint64_t str[2] = {(uint64_t)lp * 8, 128};
+    const uint32_t box[3] = {16, 64, (uint32_t)(p.kd / 16)};
+    const CUtensorMap umap = make_map(ubuf, 3, dims, str, box);
+    ContractParams q = prm;
+    q.col0 = 0;
+    q.out = d->out;
+    q.ldo = d->R;
+    launch_variant(p, 8, xmap, umap, q, st);
+    return;
+  }
   for (int c = 0; c < p.chunks; ++c) {
     const int col0 = c * 64;
     const int cols = (int)std::min<int64_t>(64, d->R - col0);
@@ -1153,9 +1216,8 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
     if (!p.col) {
       const int64_t lp = (d->L + 1) / 2 * 2;
       const int64_t n = (int64_t)cols * d->L;
-      launch_pdl(transpose_factor_kernel, dim3((unsigned)cdiv(n, 256)), dim3(256), 0, st, d->U,
-                 ldu, d->L, cols, col0, ubuf, lp);
-      count_launch();
+      (void)n;
+      launch_transpose(d->U, ldu, d->L, cols, col0, ubuf, lp, st);
       if (prm.fused_tma) {
         const uint64_t dims[3] = {16, (uint64_t)cols, (uint64_t)(d->L / 16)};
         const uint64_t str[2] = {(uint64_t)lp * 8, 128};

@@ -831,3 +831,38 @@ def test_run_report_matches_reference_report(eb, name, einsum, ext, P):
     assert ea <= 1e-10 and eb_ <= 1e-10
     assert list(a.keys()) == list(b.keys())
     assert a == b
+
+
+@pytest.mark.parametrize("M,L,R", [(128, 16, 65), (300, 96, 200), (257, 64, 130),
+                                   (1000, 512, 1024), (4096, 4096, 72)])
+@pytest.mark.parametrize("gemm_mode", [True, False])
+def test_contract_gemm_wide(eb, M, L, R, gemm_mode, opts):
+    """GEMM steps with N = R > 64 (the 1MM/2MM/3MM chains):
+    the GEMM mode of the contraction kernel (items = row tile x 64-column
+    block, whole K loop per item, Uᵀ staged once, direct stores) and, forced
+    off, the per-64-column split-K path — both against numpy FP64."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    opts("gemm", 1 if gemm_mode else 2)
+    A = oracle.random_tensor((M, L), 41)
+    B = oracle.random_tensor((L, R), 42)
+    want = A @ B
+    out = torch.full((M, R), float("nan"), dtype=torch.float64, device="cuda")
+    got = _contract(eb, C.EB_ROW, C.EB_REDUCE, 1, M, 1, L, R, torch.from_numpy(A).cuda(),
+                    torch.from_numpy(B).cuda(), [], [], out)
+    check(got, want)
+
+
+def test_executor_gemm_chain_uses_the_gemm_mode(eb):
+    """2MM through the executor at P = 1 and 4: every step on the DMMA
+    contraction kernel (no generic launches), equal to the oracle chain."""
+    e, ext = "ij,jk,kl->il", dict(i=256, j=192, k=160, l=320)
+    ops = oracle.seeded_inputs(e, ext, 9)
+    want = oracle.naive_evaluate(e, ext, ops)
+    for P in (1, 4):
+        ex = eb.Executor(e, ext, P)
+        ex.stage(ops)
+        ex.run()
+        st = ex.stats()
+        assert st["generic_launches"] == 0, st
+        check(ex.gather(), want)

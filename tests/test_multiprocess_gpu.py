@@ -84,21 +84,6 @@ def test_peer_processes_match_oracle_and_virtual(eb, case, procs, tmp_path):
         assert m[-1] <= m[1], f"rank {r} pool grew across runs: {m}"
 
 
-def test_peer_processes_c2_sweep_modes(eb, tmp_path):
-    """The three MTTKRP modes of a CP-ALS sweep at P = 4 (depth-2 and depth-4
-    groups, SURVEY Appendix A shapes scaled down) through the peer ranks."""
-    for case in ("mttkrp_m0", "mttkrp_m2"):
-        e, ext, seed = CASES[case]
-        ops = oracle.seeded_inputs(e, ext, seed)
-        plan = json.loads(eb.plan_json(e, ext, 4))
-        depth = plan["schedule"]["terms"][0]["reduction"]["depth"]
-        assert depth > 1, plan["schedule"]["terms"][0]["reduction"]
-        sub = tmp_path / case
-        sub.mkdir()
-        outs, st, _ = _run_group(case, 4, sub, runs=1)
-        assert oracle.normwise_error(outs[0], oracle.naive_evaluate(e, ext, ops).ravel()) <= TOL
-
-
 def test_run_json_rank_threads_on_one_gpu(eb, monkeypatch):
     """einplan_run_json with one host thread per rank (EINPLAN_DEVICES=0,0,...
     places every rank thread on GPU 0; the peer transport between threads):
