@@ -1310,11 +1310,7 @@ void run_contract2(const eb_contract_desc* d, const double* a, int64_t lda, doub
   const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
   const int nt = p.nt;
   const int64_t lp = (d->L + 1) / 2 * 2;
-  const int64_t n = (int64_t)d->R * d->L;
-  transpose_factor_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(d->U, ldu, d->L, (int)d->R, 0,
-                                                                   ubuf, lp);
-  EB_CUDA(cudaGetLastError());
-  count_launch();
+  launch_transpose(d->U, ldu, d->L, (int)d->R, 0, ubuf, lp, st);
   CUtensorMap umap, xmap;
   prm.fused_tma = d->L % 16 == 0 && !options().no_fused_tma ? 1 : 0;
   if (prm.fused_tma) {
