@@ -148,6 +148,18 @@ int eb_copy_box(int nd, const double* src, const int64_t* src_shape, double* dst
                 const int64_t* dst_shape, const int64_t* oy_lo, const int64_t* oy_hi,
                 const int64_t* ox_lo, void* stream);
 
+/* Row padding for the DMMA path of odd contiguous extents (TMA needs 16-byte
+ * row pitches): dst [rows][dcols] = src [rows][cols] with zero columns
+ * cols..dcols-1. */
+int eb_pad_rows(const double* src, int64_t rows, int64_t cols, double* dst, int64_t dcols,
+                void* stream);
+
+/* dst = src with its dims reordered: dst dim d is src dim perm[d] (both
+ * dense row-major; the TTM step whose result order differs from the
+ * kernel's [pre, post, b]). */
+int eb_permute(int nd, const double* src, const int64_t* src_shape, const int* perm, double* dst,
+               void* stream);
+
 /* Any dense einsum with up to 8 operands, evaluated on the device (used for
  * run(..., verify) on the GPU: the reference compares against naive_evaluate,
  * executor.cpp:255-261). */

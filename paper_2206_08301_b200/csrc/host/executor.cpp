@@ -856,19 +856,22 @@ bool ScheduleExecutor::try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
     d.Q = 1;
     for (int k = m + 1; k < N - 1; ++k) d.Q *= ext[k];
     d.L = ext[N - 1];
-    if (d.L % 2) return false;
     for (int k = 0; k < m; ++k) d.pre[d.n_pre++] = factor(k);
     for (int k = m + 1; k < N - 1; ++k) d.mid[d.n_mid++] = factor(k);
     const eb_factor u = factor(N - 1);
     d.U = u.ptr;
     d.ldu = u.ld;
+    if (d.L % 2) {  // odd contiguous extent: zero-padded X rows and U (TMA pitch)
+      d.X = padded_rows(d.X, d.P * d.M * d.Q, d.L);
+      d.U = padded_factor(u.ptr, d.L, u.ld);
+      d.L += 1;
+    }
   } else {
     d.variant = EB_COL;
     d.P = 1;
     for (int k = 0; k < N - 2; ++k) d.P *= ext[k];
     d.Q = ext[N - 2];
     d.M = ext[N - 1];
-    if (d.M % 2) return false;
     for (int k = 0; k < N - 2; ++k) d.pre[d.n_pre++] = factor(k);
     const eb_factor u = factor(N - 2);
     d.U = u.ptr;
@@ -877,11 +880,39 @@ bool ScheduleExecutor::try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
   if (d.n_pre > 8 || d.n_mid > 8) return false;
   out = new_block(term, term.placement_of(term.statement.output).indices, rank, false, true);
   d.out = out.ptr;
+  const std::int64_t M0 = d.M;
+  if (d.variant == EB_COL && d.M % 2) {  // odd contiguous (output) extent: pad, copy back
+    d.X = padded_rows(d.X, d.P * d.Q, d.M);
+    d.M += 1;
+    d.out = run_arena_.alloc(d.M * d.R, stream_, false);
+  }
   const std::size_t wb = eb_contract_workspace(&d);
   if (wb == 0) return false;
   eb_ok(eb_contract(&d, workspace(wb), wb, stream_), "eb_contract (MTTKRP term)");
+  if (d.out != out.ptr)  // rows 0..M0-1 of [M0+1][R] are the first M0*R elements
+    cuda_ok(cudaMemcpyAsync(out.ptr, d.out, static_cast<std::size_t>(M0 * d.R) * 8,
+                            cudaMemcpyDeviceToDevice, stream_),
+            "unpad");
   ++launches_fused_;
   return true;
+}
+
+const double* ScheduleExecutor::padded_rows(const double* src, std::int64_t rows,
+                                            std::int64_t cols) {
+  double* p = run_arena_.alloc(rows * (cols + 1), stream_, false);
+  eb_ok(eb_pad_rows(src, rows, cols, p, cols + 1, stream_), "eb_pad_rows");
+  return p;
+}
+
+const double* ScheduleExecutor::padded_factor(const double* u, std::int64_t rows,
+                                              std::int64_t ld) {
+  double* p = run_arena_.alloc((rows + 1) * ld, stream_, false);
+  cuda_ok(cudaMemcpyAsync(p, u, static_cast<std::size_t>(rows * ld) * 8, cudaMemcpyDeviceToDevice,
+                          stream_),
+          "pad factor");
+  cuda_ok(cudaMemsetAsync(p + rows * ld, 0, static_cast<std::size_t>(ld) * 8, stream_),
+          "pad factor");
+  return p;
 }
 
 // A term of exactly two TTM steps chained through their intermediate,
@@ -961,39 +992,75 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
     std::string want = xi;
     if (pos != std::string::npos) want.erase(pos, 1);
     want.push_back(b);
-    if (pos != std::string::npos && !contains(xi, b) && s.result_indices == want) {
+    std::string sorted_want = want, sorted_res = s.result_indices;
+    std::sort(sorted_want.begin(), sorted_want.end());
+    std::sort(sorted_res.begin(), sorted_res.end());
+    if (pos != std::string::npos && !contains(xi, b) && sorted_res == sorted_want) {
       std::int64_t P = 1, M = 1;
       for (std::size_t k = 0; k < pos; ++k) P *= local_len(term, xi[k], rank);
       for (std::size_t k = pos + 1; k < xi.size(); ++k) M *= local_len(term, xi[k], rank);
       const std::int64_t Q = local_len(term, j, rank), N = local_len(term, b, rank);
+      // the kernel writes [pre, post, b]; a result in another order (e.g. the
+      // chain's last step writing the einsum's output order) is permuted after
+      const bool permuted = s.result_indices != want;
+      double* natural = permuted ? run_arena_.alloc(P * M * N, stream_, false) : out.ptr;
       eb_contract_desc d;
       std::memset(&d, 0, sizeof(d));
       d.R = N;
       d.X = lhs->ptr;
       d.U = rhs->ptr;
       d.ldu = N;
-      d.out = out.ptr;
-      bool ok = false;
-      if (M > 1 && M % 2 == 0) {  // contract a strided mode: batched COL
+      d.out = natural;
+      bool ok = false, unpad = false;
+      if (M > 1) {  // contract a strided mode: batched COL
         d.variant = EB_COL;
         d.mode = EB_BATCHED;
         d.P = P;
         d.Q = Q;
         d.M = M;
+        if (M % 2) {  // odd contiguous extent: padded X rows, output unpadded after
+          d.X = padded_rows(d.X, P * Q, M);
+          d.M = M + 1;
+          d.out = run_arena_.alloc(P * (M + 1) * N, stream_, false);
+          unpad = true;
+        }
         ok = true;
-      } else if (M == 1 && Q % 2 == 0) {  // contract the last mode: GEMM (ROW)
+      } else {  // contract the last mode: GEMM (ROW)
         d.variant = EB_ROW;
         d.mode = EB_REDUCE;
         d.P = 1;
         d.M = P;
         d.Q = 1;
         d.L = Q;
+        if (Q % 2) {  // odd contracted extent: zero-padded rows of X and U
+          d.X = padded_rows(d.X, P, Q);
+          d.U = padded_factor(rhs->ptr, Q, N);
+          d.L = Q + 1;
+        }
         ok = true;
       }
       if (ok) {
         const std::size_t wb = eb_contract_workspace(&d);
         if (wb > 0) {
           eb_ok(eb_contract(&d, workspace(wb), wb, stream_), "eb_contract (TTM step)");
+          if (unpad) {
+            const std::int64_t sshape[3] = {P, M + 1, N}, dshape[3] = {P, M, N};
+            const std::int64_t lo[3] = {0, 0, 0}, hi[3] = {P, M, N};
+            eb_ok(eb_copy_box(3, d.out, sshape, natural, dshape, lo, hi, lo, stream_), "unpad");
+          }
+          if (permuted) {
+            // out dim k is natural dim want.find(result[k])
+            const int nd = static_cast<int>(want.size());
+            std::vector<std::int64_t> nshape(static_cast<std::size_t>(nd));
+            std::vector<int> perm(static_cast<std::size_t>(nd));
+            for (int k = 0; k < nd; ++k) {
+              nshape[static_cast<std::size_t>(k)] = local_len(term, want[static_cast<std::size_t>(k)], rank);
+              perm[static_cast<std::size_t>(k)] =
+                  static_cast<int>(want.find(s.result_indices[static_cast<std::size_t>(k)]));
+            }
+            eb_ok(eb_permute(nd, natural, nshape.data(), perm.data(), out.ptr, stream_),
+                  "eb_permute");
+          }
           ++launches_ttm_;
           return out;
         }

@@ -227,6 +227,10 @@ class ScheduleExecutor {
   // Two chained TTM steps of one term on the fused eb_ttm2 kernel.
   bool try_fused_ttm2(const TermPlan& term, std::int64_t rank,
                       const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
+  // zero-padded copies (run arena) for odd contiguous extents: X rows to
+  // cols + 1 columns, a factor [rows][ld] to rows + 1 rows
+  const double* padded_rows(const double* src, std::int64_t rows, std::int64_t cols);
+  const double* padded_factor(const double* u, std::int64_t rows, std::int64_t ld);
   DevBlock run_step(const TermPlan& term, int sid, std::int64_t rank,
                     const std::map<std::string, const DevBlock*>& at_hand);
   std::int64_t reduce(const TensorPlacement& place, const ReductionGroup& grp,

@@ -249,6 +249,90 @@ extern "C" int eb_group_sum(double* const* members, int n_members, int64_t n, vo
   });
 }
 
+namespace eb {
+// dst[r][c] = src[r][c] for c < cols, 0 for cols <= c < dcols
+__global__ void pad_rows_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
+                                double* __restrict__ dst, int64_t dcols) {
+  const int64_t n = rows * dcols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dcols, c = i - r * dcols;
+    dst[i] = c < cols ? src[r * cols + c] : 0.0;
+  }
+}
+}  // namespace eb
+
+namespace eb {
+struct PermParams {
+  int nd;
+  int64_t dshape[kMaxDim];  // destination extents
+  int64_t sstride[kMaxDim];  // source stride of each destination dim
+  int64_t n;
+  const double* src;
+  double* dst;
+};
+
+// dst (row-major, coalesced writes) gathers src through the permutation
+__global__ void permute_kernel(const PermParams p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, so = 0;
+    for (int d = p.nd - 1; d >= 0; --d) {
+      const int64_t c = r % p.dshape[d];
+      r /= p.dshape[d];
+      so += c * p.sstride[d];
+    }
+    p.dst[i] = p.src[so];
+  }
+}
+}  // namespace eb
+
+extern "C" int eb_permute(int nd, const double* src, const int64_t* src_shape, const int* perm,
+                          double* dst, void* stream) {
+  return eb::guard([&] {
+    if (nd < 1 || nd > eb::kMaxDim || !src || !dst || !src_shape || !perm)
+      throw eb::InvalidError("eb_permute: bad arguments");
+    eb::PermParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.nd = nd;
+    p.src = src;
+    p.dst = dst;
+    int64_t sst[eb::kMaxDim];
+    int64_t acc = 1;
+    for (int d = nd - 1; d >= 0; --d) {
+      sst[d] = acc;
+      acc *= src_shape[d];
+    }
+    unsigned seen = 0;
+    p.n = 1;
+    for (int d = 0; d < nd; ++d) {
+      if (perm[d] < 0 || perm[d] >= nd || (seen >> perm[d]) & 1u)
+        throw eb::InvalidError("eb_permute: not a permutation");
+      seen |= 1u << perm[d];
+      p.dshape[d] = src_shape[perm[d]];
+      p.sstride[d] = sst[perm[d]];
+      p.n *= p.dshape[d];
+    }
+    if (p.n == 0) return;
+    eb::permute_kernel<<<eb::grid_for(p.n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    EB_CUDA(cudaGetLastError());
+    eb::count_launch();
+  });
+}
+
+extern "C" int eb_pad_rows(const double* src, int64_t rows, int64_t cols, double* dst,
+                           int64_t dcols, void* stream) {
+  return eb::guard([&] {
+    if (!src || !dst || rows < 0 || cols < 0 || dcols < cols)
+      throw eb::InvalidError("eb_pad_rows: bad arguments");
+    if (rows * dcols == 0) return;
+    eb::pad_rows_kernel<<<eb::grid_for(rows * dcols, 256), 256, 0,
+                          static_cast<cudaStream_t>(stream)>>>(src, rows, cols, dst, dcols);
+    EB_CUDA(cudaGetLastError());
+    eb::count_launch();
+  });
+}
+
 extern "C" int eb_group_sum_into(const double* const* members, int n_members, int64_t n,
                                  double* dst, void* stream) {
   return eb::guard([&] {

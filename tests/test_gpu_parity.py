@@ -555,11 +555,13 @@ def test_run_json_tensor_files(eb, tmp_path, fmt):
     check(np.asarray(got).reshape(40, 12), oracle.naive_evaluate(e, ext, ops))
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_einsums_match_oracle(eb, seed):
-    """Randomised parity: random MTTKRP / TTMc einsums, extents and P through
-    the executor (fused kernels, TTM steps, generic fallbacks, reductions and
-    redistributions on virtual ranks) against the oracle's naive loop."""
+    """Randomised parity: random MTTKRP / TTMc einsums, extents (odd and
+    ragged) and P through the executor (fused kernels, TTM steps, padded odd
+    extents, permuted TTM results, reductions and redistributions on virtual
+    ranks) against the oracle's naive loop.  With every extent >= 2 no step
+    may fall back to the generic (non-tensor-core) kernel."""
     rng = np.random.default_rng(1000 + seed)
     e, ext, P = _random_case(rng)
     ops = oracle.seeded_inputs(e, ext, seed)
@@ -568,6 +570,8 @@ def test_random_einsums_match_oracle(eb, seed):
     ex.stage(ops)
     ex.run()
     check(ex.gather(), want)
+    if min(ext.values()) >= 2:
+        assert ex.stats()["generic_launches"] == 0, (e, ext, P, ex.stats())
 
 
 @pytest.mark.parametrize("name,einsum,ext", DESK, ids=[d[0] for d in DESK])
@@ -866,3 +870,27 @@ def test_executor_gemm_chain_uses_the_gemm_mode(eb):
         st = ex.stats()
         assert st["generic_launches"] == 0, st
         check(ex.gather(), want)
+
+
+@pytest.mark.parametrize("e,ext", [
+    ("ijk,ja,ka->ia", dict(i=40, j=36, k=35, a=24)),      # ROW, odd contracted extent
+    ("ijk,ia,ka->ja", dict(i=30, j=130, k=17, a=8)),      # ROW mode 1, odd L
+    ("ijk,ia,ja->ka", dict(i=12, j=10, k=137, a=24)),     # COL, odd output extent
+    ("ijk,jb,kc->ibc", dict(i=20, j=31, k=33, b=8, c=5)),  # TTMs with odd extents
+    ("ijkl,jb,kc,ld->ibcd", dict(i=8, j=11, k=2, l=7, b=2, c=3, d=5)),  # permuted results
+    ("ij,jk,kl->il", dict(i=33, j=35, k=37, l=39)),       # GEMM chain, odd everything
+])
+@pytest.mark.parametrize("P", [1, 4])
+def test_odd_extents_stay_on_the_dmma_path(eb, e, ext, P):
+    """Odd contiguous extents are zero-padded (TMA needs 16-byte pitches) and
+    TTM results in another index order are permuted after the kernel: no step
+    falls back to the generic kernel, and the result equals the oracle's."""
+    ops = oracle.seeded_inputs(e, ext, 51)
+    want = oracle.naive_evaluate(e, ext, ops)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    ex.run()
+    st = ex.stats()
+    assert st["generic_launches"] == 0, st
+    assert st["fused_launches"] + st["ttm_launches"] > 0, st
+    check(ex.gather(), want)

@@ -67,6 +67,7 @@ assert bool(torch.isfinite(A).all())
 
 # the peer transport between rank threads on one GPU
 os.environ["EINPLAN_DEVICES"] = "0,0,0,0"
+os.environ["EINPLAN_MAX_POINTS"] = "1000000000"
 st, rep = eb.Session("ijk,jb,kc->ibc", dict(i=96, j=96, k=96, b=24, c=24)).run_json(4, seed=2)
 del os.environ["EINPLAN_DEVICES"]
 r = json.loads(rep)
