@@ -38,15 +38,22 @@ CASES = {
 
 
 def main():
+    import time
     case, procs, rank, group, outdir, runs = sys.argv[1:7]
     procs, rank, runs = int(procs), int(rank), int(runs)
     e, ext, seed = CASES[case]
+    t0 = time.perf_counter()
+    log = lambda what: print(f"rank {rank} {what} {time.perf_counter() - t0:.3f}s", flush=True)
     ex = eb.Executor(e, ext, procs, rank=rank, transport="peer", group=group)
+    log("created")
     ex.stage(oracle.seeded_inputs(e, ext, seed))
+    log("staged")
     mem = []
     for r in range(runs):
         ex.run()
+        log(f"run {r}")
         out = ex.gather()
+        log(f"gather {r}")
         mem.append(eb.mem_in_use())
         if rank == 0:
             np.save(os.path.join(outdir, f"out{r}.npy"), out)
