@@ -78,6 +78,26 @@ size_t eb_contract_workspace(const eb_contract_desc* d);
 int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,
                 void* stream);
 
+/* Output scatter: the redistribution of a term's output fused into the
+ * producing kernel's epilogue (a "push": apply_plan's message boxes,
+ * redistribute.cpp:51-148 / 185-206, realised element by element).  Instead
+ * of its dense output block the kernel stores every element straight into
+ * the destination block(s) of the next term's placement — on the same
+ * device (virtual ranks) or in the peers' mapped exchange heaps (NVLink
+ * stores).  The kernel's natural output block is row-major over nd dims:
+ * [0, n_outer) form its outer index, [n_outer, n_outer + n_row) its row, the
+ * rest its column.  Dim d has local extent ext[d] and global base gbase[d];
+ * the element at global coordinates g goes to destination rank
+ *   sum_d (g_d / block[d]) * rank_stride[d] + rep_offset[k]   (k < n_rep)
+ * at element offset sum_d (g_d % block[d]) * local_stride[d] of dest[rank].
+ * Every coordinate and extent must be below 2^31. */
+typedef struct eb_scatter {
+  int nd, n_outer, n_row, n_rep;
+  int64_t ext[8], gbase[8], block[8], rank_stride[8], local_stride[8];
+  int64_t rep_offset[8];
+  double* dest[64];
+} eb_scatter;
+
 /* Dimension-tree pair (CP-ALS sweep, order 3): one pass over X computes the
  * mode-0 MTTKRP (d: EB_ROW, EB_REDUCE, P = 1, one `mid` factor B, U = C) and
  * the mode-1 MTTKRP  out1[j][r] = sum_{i,k} X[i,j,k] A[i,r] C[k,r]:
@@ -119,6 +139,13 @@ typedef struct eb_ttm2_desc {
 } eb_ttm2_desc;
 
 int eb_ttm2(const eb_ttm2_desc* d, void* stream);
+
+/* eb_contract (EB_COL, EB_BATCHED only) / eb_ttm2 with the scatter epilogue;
+ * d->out is ignored. */
+int eb_contract_scatter(const eb_contract_desc* d, const eb_scatter* s, void* workspace,
+                        size_t workspace_bytes, void* stream);
+int eb_ttm2_scatter(const eb_ttm2_desc* d, const eb_scatter* s, void* stream);
+
 
 /* Generic binary (or unary) einsum step on dense row-major device blocks:
  * out[...] = sum over contracted symbols of lhs[...] * rhs[...] — the GPU
@@ -197,7 +224,9 @@ int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fas
  * call changes them between runs): "no_fused_tma" 0/1, "no_rf" 0/1,
  * "rf_cfg" "RTxOS"|"auto", "ttm2_variant" 0/1/2, "fuse_ttm2" 0/1,
  * "gemm" 0 auto / 1 forced / 2 off (wide GEMM steps: one launch over
- * (row tile, 64-column block) items instead of per-64-column split-K). */
+ * (row tile, 64-column block) items instead of per-64-column split-K),
+ * "fuse_redistribution" 0/1 (TTM outputs pushed by the producing kernel into
+ * the next term's blocks, eb_scatter). */
 int eb_set_option(const char* name, const char* value);
 
 /* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------
@@ -268,6 +297,9 @@ int64_t eb_exec_output_elems(eb_exec* h);
  *         fused MTTKRP launches, TTM/GEMM launches, generic launches,
  *         tree flops, terms} of the last run */
 int eb_exec_stats(eb_exec* h, int64_t* out8);
+/* how many redistributions of the last run were fused into their producer
+ * (pushed by the TTM epilogue, eb_scatter) */
+int eb_exec_fused_redistributions(eb_exec* h);
 /* run_report JSON of the last run (output sum from host_out, may be NULL) */
 int eb_exec_report_json(eb_exec* h, const double* host_out, char** json_out);
 

@@ -364,7 +364,9 @@ class Executor:
         _capi.check(_capi.lib().eb_exec_stats(self._h, v))
         keys = ["allreduce_volume", "redistribute_volume", "max_rank_sent", "fused_launches",
                 "ttm_launches", "generic_launches", "tree_flops", "terms"]
-        return dict(zip(keys, list(v)))
+        d = dict(zip(keys, list(v)))
+        d["fused_redistributions"] = int(_capi.lib().eb_exec_fused_redistributions(self._h))
+        return d
 
     def report_json(self, out: np.ndarray | None = None) -> str:
         p = ctypes.c_void_p()

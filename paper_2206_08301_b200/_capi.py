@@ -59,7 +59,8 @@ EXPORTS = [
     "eb_cp3_als_workspace", "eb_cp3_als_sweep",
     "eb_step_generic",
     "eb_group_sum", "eb_group_sum_into", "eb_copy_box", "eb_set_option", "eb_exec_create_peer",
-    "eb_exec_stage_region", "eb_rng_create", "eb_rng_fill", "eb_rng_destroy", "eb_mem_in_use", "eb_pad_rows", "eb_permute", "eb_einsum_generic", "eb_random_fill_host",
+    "eb_exec_stage_region", "eb_rng_create", "eb_rng_fill", "eb_rng_destroy", "eb_mem_in_use", "eb_pad_rows", "eb_permute",
+    "eb_contract_scatter", "eb_ttm2_scatter", "eb_exec_fused_redistributions", "eb_einsum_generic", "eb_random_fill_host",
     "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
@@ -151,6 +152,8 @@ def lib():
         _sig(L, "eb_rng_fill", None, [_vp, _dp, _i64])
         _sig(L, "eb_rng_destroy", None, [_vp])
         _sig(L, "eb_mem_in_use", ctypes.c_int, [ctypes.POINTER(_i64)])
+        _sig(L, "eb_exec_fused_redistributions", ctypes.c_int, [_vp])
+        _sig(L, "eb_ttm2_scatter", ctypes.c_int, [ctypes.POINTER(Ttm2Desc), _vp, _vp])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,
              [c, c, _i64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(_vp)])

@@ -572,6 +572,10 @@ int eb_exec_stats(eb_exec* h, int64_t* out8) {
   });
 }
 
+int eb_exec_fused_redistributions(eb_exec* h) {
+  return h ? h->exec->redistributions_fused() : -1;
+}
+
 int eb_exec_report_json(eb_exec* h, const double* host_out, char** json_out) {
   return exec_guard([&] {
     SimulationReport sim;

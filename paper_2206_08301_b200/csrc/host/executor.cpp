@@ -794,6 +794,14 @@ void ScheduleExecutor::prepare_heap() {
     heap_slot_[t.index] = off;
     off += (static_cast<std::size_t>(most) * 8 + 255) / 256 * 256;
   }
+  heap_in_slot_.clear();
+  for (const TermPlan& t : terms)
+    if (const RedistRecord* rec = push_record(t)) {  // fused redistribution target
+      std::int64_t n = 1;
+      for (auto bsz : rec->plan.destination.dist.blocks) n *= bsz;
+      heap_in_slot_[rec->to_term] = off;
+      off += (static_cast<std::size_t>(n) * 8 + 255) / 256 * 256;
+    }
   // identical on every rank (same schedule), so the decision is collective
   if (off <= heap_bytes_) return;
   cuda_ok(cudaStreamSynchronize(stream_), "heap: sync");
@@ -919,9 +927,8 @@ const double* ScheduleExecutor::padded_factor(const double* u, std::int64_t rows
 //   s0: X[P j k R], U1[j b] -> t0[P k R b]    s1: t0[P k R b], U2[k c] -> out[P R b c]
 // (both TTMc-O5 terms; executor.cpp:220-235 runs them back to back) goes to
 // eb_ttm2 with t0 kept on chip.
-bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
-                                      const std::map<std::string, const DevBlock*>& at_hand,
-                                      DevBlock& out) {
+bool ScheduleExecutor::ttm2_shape(const TermPlan& term, std::int64_t rank, eb_ttm2_desc& d,
+                                  std::string& natural, int& n_pre, int& n_rest) const {
   if (term.step_ids.size() != 2) return false;
   const ContractionTree& tree = pipe_.tree;
   const ContractionStep& s0 = tree.steps[static_cast<std::size_t>(term.step_ids[0])];
@@ -941,17 +948,32 @@ bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
   if (s0.result_indices != pre + k + rest + b || s1.lhs_indices != s0.result_indices ||
       s1.result_indices != pre + rest + b + c)
     return false;
-  eb_ttm2_desc d;
   std::memset(&d, 0, sizeof(d));
   d.P = 1;
-  for (char s : pre) d.P *= local_len(term, s, rank);
+  for (char sy : pre) d.P *= local_len(term, sy, rank);
   d.M = 1;
-  for (char s : rest) d.M *= local_len(term, s, rank);
+  for (char sy : rest) d.M *= local_len(term, sy, rank);
   d.Q1 = local_len(term, j, rank);
   d.Q2 = local_len(term, k, rank);
   d.N1 = local_len(term, b, rank);
   d.N2 = local_len(term, c, rank);
   if (d.Q1 > 64 || d.N1 > 16 || d.N2 > 16 || d.M % 2 != 0) return false;
+  natural = s1.result_indices;
+  n_pre = static_cast<int>(pre.size());
+  n_rest = static_cast<int>(rest.size());
+  return true;
+}
+
+bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
+                                      const std::map<std::string, const DevBlock*>& at_hand,
+                                      DevBlock& out) {
+  eb_ttm2_desc d;
+  std::string natural;
+  int n_pre = 0, n_rest = 0;
+  if (!ttm2_shape(term, rank, d, natural, n_pre, n_rest)) return false;
+  const ContractionTree& tree = pipe_.tree;
+  const ContractionStep& s0 = tree.steps[static_cast<std::size_t>(term.step_ids[0])];
+  const ContractionStep& s1 = tree.steps[static_cast<std::size_t>(term.step_ids[1])];
   const DevBlock* x = at_hand.at(tree.tensor_name(s0.lhs));
   const DevBlock* u1 = at_hand.at(tree.tensor_name(s0.rhs));
   const DevBlock* u2 = at_hand.at(tree.tensor_name(s1.rhs));
@@ -960,11 +982,138 @@ bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
   d.ldu1 = u1->shape[1];
   d.U2 = u2->ptr;
   d.ldu2 = u2->shape[1];
-  out = new_block(term, s1.result_indices, rank, false, true);
-  d.out = out.ptr;
-  eb_ok(eb_ttm2(&d, stream_), "eb_ttm2 (fused TTM pair)");
+  if (push_rec_) {  // fused redistribution: the epilogue stores into the next term's blocks
+    eb_scatter sc;
+    scatter_desc(term, rank, natural, n_pre, n_rest, sc);
+    out = DevBlock{};
+    eb_ok(eb_ttm2_scatter(&d, &sc, stream_), "eb_ttm2_scatter (fused TTM pair + redistribution)");
+  } else {
+    out = new_block(term, s1.result_indices, rank, false, true);
+    d.out = out.ptr;
+    eb_ok(eb_ttm2(&d, stream_), "eb_ttm2 (fused TTM pair)");
+  }
   ++launches_fused_;
   return true;
+}
+
+namespace {
+bool uniform_blocks(const TensorPlacement& pl) {
+  for (std::size_t d = 0; d < pl.indices.size(); ++d) {
+    const std::int64_t g = pl.term_grid.dims[static_cast<std::size_t>(pl.axes[d])];
+    if (pl.dist.blocks[d] * g != pl.dist.extents[d]) return false;
+    if (pl.dist.extents[d] >= (std::int64_t(1) << 31)) return false;
+  }
+  return true;
+}
+}  // namespace
+
+const RedistRecord* ScheduleExecutor::push_record(const TermPlan& t) const {
+  if (!eb::options().fuse_redistribution || t.reduction.depth > 1) return nullptr;
+  // the producer stores into every destination block: all of them must be
+  // addressable here (one device, or the peers' mapped heaps — not NCCL)
+  if (!transport_->is_virtual() && !transport_->peer_mapped()) return nullptr;
+  const RedistRecord* rec = nullptr;
+  for (const RedistRecord& r : pipe_.schedule.redistributions)
+    if (r.from_term == t.index && r.tensor == t.statement.output) rec = &r;
+  if (!rec || pipe_.schedule.procs > 64) return nullptr;
+  const TensorPlacement& src = t.placement_of(t.statement.output);
+  const TensorPlacement& dst = rec->plan.destination;
+  if (!uniform_blocks(src) || !uniform_blocks(dst)) return nullptr;
+  std::int64_t reps = 1;
+  for (std::size_t a = 0; a < dst.term_grid.dims.size(); ++a)
+    if (std::find(dst.axes.begin(), dst.axes.end(), static_cast<int>(a)) == dst.axes.end())
+      reps *= dst.term_grid.dims[a];
+  if (reps > 8) return nullptr;
+  if (match_mttkrp(t.statement).ok) return nullptr;
+  // uniform source blocks: every rank's producing step has the same shape,
+  // so rank 0 decides for all (and every process decides alike)
+  eb_ttm2_desc d;
+  std::string natural;
+  int n_pre = 0, n_rest = 0;
+  if (eb::options().fuse_ttm2 && ttm2_shape(t, 0, d, natural, n_pre, n_rest)) return rec;
+  const ContractionStep& s = pipe_.tree.steps[static_cast<std::size_t>(t.step_ids.back())];
+  if (s.rhs < 0 || s.rhs_indices.size() != 2) return nullptr;
+  const std::string& xi = s.lhs_indices;
+  const char j = s.rhs_indices[0], b = s.rhs_indices[1];
+  const auto pos = xi.find(j);
+  if (pos == std::string::npos || contains(xi, b)) return nullptr;
+  std::string want = xi;
+  want.erase(pos, 1);
+  want.push_back(b);
+  std::string sw = want, sr = s.result_indices;
+  std::sort(sw.begin(), sw.end());
+  std::sort(sr.begin(), sr.end());
+  if (sw != sr) return nullptr;
+  std::int64_t M = 1;
+  for (std::size_t k = pos + 1; k < xi.size(); ++k) M *= local_len(t, xi[k], 0);
+  if (M < 2 || M % 2) return nullptr;  // the COL BATCHED kernel without padding
+  return rec;
+}
+
+void ScheduleExecutor::scatter_desc(const TermPlan& term, std::int64_t rank,
+                                    const std::string& natural, int n_outer, int n_row,
+                                    eb_scatter& sc) const {
+  const TensorPlacement& dst = push_rec_->plan.destination;
+  std::memset(&sc, 0, sizeof(sc));
+  sc.nd = static_cast<int>(natural.size());
+  sc.n_outer = n_outer;
+  sc.n_row = n_row;
+  const std::size_t ng = dst.term_grid.dims.size();
+  std::vector<std::int64_t> gstride(ng, 1);
+  for (std::size_t a = ng; a-- > 1;) gstride[a - 1] = gstride[a] * dst.term_grid.dims[a];
+  for (int d = 0; d < sc.nd; ++d) {
+    const char sym = natural[static_cast<std::size_t>(d)];
+    const auto t = dst.indices.find(sym);
+    if (t == std::string::npos) fail(errc::invalid_argument, "scatter: symbol not in destination");
+    sc.ext[d] = local_len(term, sym, rank);
+    sc.gbase[d] = local_lo(term, sym, rank);
+    sc.block[d] = dst.dist.blocks[t];
+    sc.rank_stride[d] = gstride[static_cast<std::size_t>(dst.axes[t])];
+    std::int64_t ls = 1;
+    for (std::size_t u = t + 1; u < dst.indices.size(); ++u) ls *= dst.dist.blocks[u];
+    sc.local_stride[d] = ls;
+  }
+  // replicas: every combination of the destination grid axes the tensor does not span
+  std::vector<std::int64_t> reps{0};
+  for (std::size_t a = 0; a < ng; ++a) {
+    if (std::find(dst.axes.begin(), dst.axes.end(), static_cast<int>(a)) != dst.axes.end())
+      continue;
+    std::vector<std::int64_t> next;
+    for (std::int64_t r0 : reps)
+      for (std::int64_t c = 0; c < dst.term_grid.dims[a]; ++c) next.push_back(r0 + c * gstride[a]);
+    reps.swap(next);
+  }
+  sc.n_rep = static_cast<int>(reps.size());
+  for (std::size_t k = 0; k < reps.size(); ++k) sc.rep_offset[k] = reps[k];
+  for (std::int64_t r = 0; r < pipe_.schedule.procs; ++r)
+    sc.dest[r] = push_dst_[static_cast<std::size_t>(r)].ptr;
+}
+
+void ScheduleExecutor::arm_push() {
+  const TensorPlacement& dst = push_rec_->plan.destination;
+  const std::int64_t procs = pipe_.schedule.procs;
+  const bool peer = transport_->peer_mapped();
+  if (peer) {
+    // no rank may still read its destination block from the previous run
+    cuda_ok(cudaStreamSynchronize(stream_), "push: sync");
+    static_cast<PeerTransport*>(transport_)->comm().barrier();
+  }
+  push_dst_.assign(static_cast<std::size_t>(procs), DevBlock{});
+  const std::size_t off = heap_in_slot_.count(push_rec_->to_term) ? heap_in_slot_.at(push_rec_->to_term) : 0;
+  for (std::int64_t r = 0; r < procs; ++r) {
+    DevBlock& b = push_dst_[static_cast<std::size_t>(r)];
+    const auto bc = dst.block_coords_of(r);
+    b.shape = dst.dist.shape_of(bc);
+    b.base = dst.dist.base_of(bc);
+    if (peer) {
+      char* base = heap_peers_[static_cast<std::size_t>(r)];
+      if (!base || !heap_in_slot_.count(push_rec_->to_term))
+        fail(errc::invalid_argument, "push: destination heap not mapped");
+      b.ptr = reinterpret_cast<double*>(base + off);
+    } else if (transport_->owns(r)) {
+      b.ptr = run_arena_.alloc(prod(b.shape), stream_, false);
+    }
+  }
 }
 
 DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t rank,
@@ -980,7 +1129,9 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
   };
   const bool is_output =
       tree.tensor_name(tree.result_id(sid)) == term.statement.output;
-  DevBlock out = new_block(term, s.result_indices, rank, false, is_output);
+  // with a fused redistribution armed the output step writes no block of its own
+  const bool pushing = is_output && push_rec_ != nullptr;
+  DevBlock out = pushing ? DevBlock{} : new_block(term, s.result_indices, rank, false, is_output);
   const DevBlock* lhs = operand(s.lhs);
   const DevBlock* rhs = s.rhs >= 0 ? operand(s.rhs) : nullptr;
 
@@ -1003,7 +1154,8 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
       // the kernel writes [pre, post, b]; a result in another order (e.g. the
       // chain's last step writing the einsum's output order) is permuted after
       const bool permuted = s.result_indices != want;
-      double* natural = permuted ? run_arena_.alloc(P * M * N, stream_, false) : out.ptr;
+      double* natural =
+          permuted && !pushing ? run_arena_.alloc(P * M * N, stream_, false) : out.ptr;
       eb_contract_desc d;
       std::memset(&d, 0, sizeof(d));
       d.R = N;
@@ -1012,6 +1164,26 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
       d.ldu = N;
       d.out = natural;
       bool ok = false, unpad = false;
+      if (M > 1 && pushing && M % 2 == 0) {
+        // fused redistribution: the epilogue stores the natural [pre, post, b]
+        // elements straight into the next term's destination blocks
+        d.variant = EB_COL;
+        d.mode = EB_BATCHED;
+        d.P = P;
+        d.Q = Q;
+        d.M = M;
+        eb_scatter sc;
+        scatter_desc(term, rank, want, static_cast<int>(pos),
+                     static_cast<int>(xi.size() - pos - 1), sc);
+        const std::size_t wb = eb_contract_workspace(&d);
+        if (wb == 0) fail(errc::invalid_argument, "scatter TTM: no contraction plan");
+        eb_ok(eb_contract_scatter(&d, &sc, workspace(wb), wb, stream_),
+              "eb_contract_scatter (TTM step + redistribution)");
+        ++launches_ttm_;
+        return DevBlock{};
+      }
+      if (pushing)
+        fail(errc::invalid_argument, "fused redistribution: the output step has no scatter path");
       if (M > 1) {  // contract a strided mode: batched COL
         d.variant = EB_COL;
         d.mode = EB_BATCHED;
@@ -1067,6 +1239,8 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
       }
     }
   }
+  if (pushing)
+    fail(errc::invalid_argument, "fused redistribution: the output step has no scatter path");
   std::int64_t ext[256] = {0};
   for (char c : s.lhs_indices) ext[static_cast<unsigned char>(c)] = local_len(term, c, rank);
   for (char c : s.rhs_indices) ext[static_cast<unsigned char>(c)] = local_len(term, c, rank);
@@ -1113,7 +1287,10 @@ void ScheduleExecutor::execute() {
   comm_ = CommStats{};
   comm_.per_rank_sent.assign(static_cast<std::size_t>(pipe_.schedule.procs), 0);
   launches_fused_ = launches_ttm_ = launches_generic_ = 0;
+  redistributions_fused_ = 0;
   const std::int64_t procs = pipe_.schedule.procs;
+  pushed_.clear();
+  push_rec_ = nullptr;
   prepare_heap();
 
   for (const TermPlan& term : pipe_.schedule.terms) {
@@ -1125,6 +1302,17 @@ void ScheduleExecutor::execute() {
         continue;
       }
       if (const RedistRecord* rec = find_redist(term.index, a.tensor)) {
+        if (pushed_.count({term.index, a.tensor})) {
+          // fused into the producer's epilogue (push): only the accounting
+          // of apply_plan remains (redistribute.cpp:185-206, executor.cpp:193-198)
+          comm_.events.push_back(
+              {"redistribute", term.index, a.tensor, rec->plan.transmitted_volume});
+          comm_.redistribute_volume += rec->plan.transmitted_volume;
+          for (const Message& m : rec->plan.messages)
+            if (!m.self) comm_.per_rank_sent[static_cast<std::size_t>(m.src_rank)] += m.elements;
+          arrays[a.tensor] = &store_.at({term.index, a.tensor});
+          continue;
+        }
         const auto& src = store_.at({rec->from_term, a.tensor});
         std::vector<DevBlock> dst(static_cast<std::size_t>(procs));
         const TensorPlacement& dp = rec->plan.destination;
@@ -1183,6 +1371,8 @@ void ScheduleExecutor::execute() {
 
     const TensorPlacement& out_place = term.placement_of(term.statement.output);
     std::vector<DevBlock> out_blocks(static_cast<std::size_t>(procs));
+    push_rec_ = push_record(term);
+    if (push_rec_) arm_push();
     for (std::int64_t rank : owned_) {
       std::map<std::string, const DevBlock*> at_hand;
       for (auto& kv : arrays) at_hand[kv.first] = &(*kv.second)[static_cast<std::size_t>(rank)];
@@ -1203,6 +1393,16 @@ void ScheduleExecutor::execute() {
           at_hand[name] = &scratch[name];
         }
       }
+    }
+    if (push_rec_) {  // the term's output is already in the next term's blocks
+      if (transport_->peer_mapped()) {
+        cuda_ok(cudaStreamSynchronize(stream_), "push: sync");
+        static_cast<PeerTransport*>(transport_)->comm().barrier();  // every block complete
+      }
+      store_[{push_rec_->to_term, push_rec_->tensor}] = push_dst_;
+      pushed_.insert({push_rec_->to_term, push_rec_->tensor});
+      ++redistributions_fused_;
+      push_rec_ = nullptr;
     }
     map_peer_blocks(term, out_blocks);
     const std::int64_t v = reduce(out_place, term.reduction, out_blocks,

@@ -204,6 +204,8 @@ class ScheduleExecutor {
   int launches_fused() const { return launches_fused_; }
   int launches_ttm() const { return launches_ttm_; }
   int launches_generic() const { return launches_generic_; }
+  // redistributions of the last run fused into their producer's epilogue
+  int redistributions_fused() const { return redistributions_fused_; }
   cudaStream_t stream() const { return stream_; }
 
  private:
@@ -222,6 +224,18 @@ class ScheduleExecutor {
   // rank computes the same offsets; (re)allocated collectively.
   void prepare_heap();
   void map_peer_blocks(const TermPlan& term, std::vector<DevBlock>& blocks);
+  // The fused TTM pair of a term (shape only: pointers unset), its natural
+  // output index order and the pre / rest dim counts; false if not that shape.
+  bool ttm2_shape(const TermPlan& term, std::int64_t rank, eb_ttm2_desc& d, std::string& natural,
+                  int& n_pre, int& n_rest) const;
+  // Fused redistribution ("push"): the record of term t's output when its
+  // producing kernel can store straight into the next term's blocks (depth-1
+  // term, uniform source and destination blocks, a TTM / TTM-pair producer),
+  // else nullptr.  A function of the schedule only: every rank agrees.
+  const RedistRecord* push_record(const TermPlan& t) const;
+  void arm_push();  // destination blocks of every rank (push_dst_)
+  void scatter_desc(const TermPlan& term, std::int64_t rank, const std::string& natural,
+                    int n_outer, int n_row, eb_scatter& sc) const;
   bool try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
                         const std::map<std::string, const DevBlock*>& at_hand, DevBlock& out);
   // Two chained TTM steps of one term on the fused eb_ttm2 kernel.
@@ -249,6 +263,7 @@ class ScheduleExecutor {
   std::size_t workspace_bytes_ = 0;
   CommStats comm_;
   int launches_fused_ = 0, launches_ttm_ = 0, launches_generic_ = 0;
+  int redistributions_fused_ = 0;
   bool async_reduce_ = false, comm_pending_ = false;
   cudaEvent_t ev_compute_ = nullptr, ev_comm_ = nullptr;
   // exchange heap (PeerTransport only)
@@ -256,6 +271,11 @@ class ScheduleExecutor {
   std::size_t heap_bytes_ = 0;
   std::vector<char*> heap_peers_;
   std::map<int, std::size_t> heap_slot_;  // term index -> byte offset
+  std::map<int, std::size_t> heap_in_slot_;  // term index -> its pushed input block
+  // fused redistribution state of the term being executed / done this run
+  const RedistRecord* push_rec_ = nullptr;
+  std::vector<DevBlock> push_dst_;
+  std::set<std::pair<int, std::string>> pushed_;
 };
 
 }  // namespace gpu

@@ -43,6 +43,7 @@ Options read_env() {
   if (const char* v = std::getenv("EB_TTM2_VARIANT")) o.ttm2_variant = std::atoi(v);
   if (const char* v = std::getenv("EB_FUSE_TTM2")) o.fuse_ttm2 = v[0] != '0';
   if (const char* v = std::getenv("EB_GEMM")) o.gemm = std::atoi(v);
+  if (const char* v = std::getenv("EB_FUSE_REDIST")) o.fuse_redistribution = v[0] != '0';
   return o;
 }
 
@@ -108,6 +109,8 @@ extern "C" int eb_set_option(const char* name, const char* value) {
       o.ttm2_variant = v;
     } else if (!std::strcmp(name, "fuse_ttm2")) {
       o.fuse_ttm2 = v != 0;
+    } else if (!std::strcmp(name, "fuse_redistribution")) {
+      o.fuse_redistribution = v != 0;
     } else if (!std::strcmp(name, "gemm")) {
       if (v < 0 || v > 2) throw eb::InvalidError("eb_set_option: gemm is 0, 1 or 2");
       o.gemm = v;

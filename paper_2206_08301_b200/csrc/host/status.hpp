@@ -69,6 +69,7 @@ struct Options {
   int ttm2_variant = 0;   // 0 auto, 1 / 2 = ttm2_ws_kernel<1> / <2>
   int fuse_ttm2 = 1;      // executor: TTM pairs on eb_ttm2 (0: two eb_contract launches)
   int gemm = 0;           // wide GEMM steps: 0 auto, 1 GEMM mode forced, 2 split-K chunks
+  int fuse_redistribution = 1;  // executor: push TTM outputs into the next term's blocks
 };
 const Options& options();
 

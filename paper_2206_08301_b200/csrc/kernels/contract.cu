@@ -76,6 +76,9 @@ struct ContractParams {
   // one TMA box per operand per stage: the 16-wide column blocks are a tensor
   // dimension of the maps (contiguous extent a multiple of 16)
   int fused_tma;
+  // BATCHED COL: scatter epilogue (sc.nd > 0) — stores go to the next term's
+  // destination blocks instead of `out`
+  eb_scatter sc;
 };
 
 __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col) {
@@ -270,6 +273,41 @@ __device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
   }
 }
 
+// BATCHED scatter epilogue: the unit (row tile mt, outer index o) stored
+// element by element into the destination blocks (eb_scatter): the outer and
+// row parts of the destination address are resolved once per unit / row,
+// the column part per element; accumulators cleared.
+template <int MI, int NT, int MT, int WM, bool VC>
+__device__ __forceinline__ void scatter_unit(double (&acc)[MI][NT][2], const ContractParams& prm,
+                                             int64_t mt, int64_t o, int wm, int g, int l) {
+  const eb_scatter& s = prm.sc;
+  int64_t ro = 0, oo = 0;
+  scatter_part(s, 0, s.n_outer, o, ro, oo);
+  const int dr = s.n_outer, dc = s.n_outer + s.n_row;
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int64_t row = mt * MT + wm * WM + (VC ? vc_row(i, g) : i * 8 + g);
+    if (row < prm.M) {
+      int64_t rm = ro, om = oo;
+      scatter_part(s, dr, dc, row, rm, om);
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = VC ? 16 * (j >> 1) + 4 * l + 2 * e + (j & 1) : j * 8 + 2 * l + e;
+          const int64_t gc = prm.col0 + c;
+          if (gc < prm.R) {
+            int64_t rk = rm, of = om;
+            scatter_part(s, dc, s.nd, gc, rk, of);
+            scatter_store(s, rk, of, acc[i][j][e]);
+          }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+}
+
 // Warp roles:
 //   warp NCW       producer: lane 0 fills the stage ring with TMA boxes of X
 //                  and U; all 32 lanes write the stage's Khatri-Rao row
@@ -293,7 +331,7 @@ __device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
 // nothing from it (measured), so only TWO uses it.  The setmaxnreg calls sit
 // inside the role branches so ptxas budgets each region separately.
 template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
-          bool DIR = false, bool WS = false>
+          bool DIR = false, bool WS = false, bool SC = false>
 __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
@@ -309,6 +347,7 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
   // from one 16-B load (see vc_row)
   constexpr bool VC = COL && MI % 2 == 0 && NT % 2 == 0;
   static_assert(!BATCHED || KS == 1, "BATCHED writes each unit once");
+  static_assert(!SC || (COL && BATCHED), "the scatter epilogue is for BATCHED COL units");
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[S];
@@ -724,6 +763,10 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
     }
+    if constexpr (SC) {  // fused redistribution: push to the destination blocks
+      scatter_unit<MI, NT, MT, WM, VC>(acc, prm, mt, o, wm, g, l);
+      continue;
+    }
     if constexpr (BATCHED && VC) {
       // out[p][m][col0 + n] from the interleaved tiles (see vc_row)
 #pragma unroll
@@ -1060,11 +1103,11 @@ Plan plan_of(const eb_contract_desc* d) {
 }
 
 template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT, bool TWO = false,
-          bool DIR = false, bool WS = false>
+          bool DIR = false, bool WS = false, bool SC = false>
 void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
               cudaStream_t st) {
   using T = Tile<COL, NWM * WM, NT, KD, OS>;
-  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR, WS>;
+  auto kern = contract_kernel<COL, BATCHED, NWM, WM, KS, KD, OS, NT, TWO, DIR, WS, SC>;
   set_smem_once(kern, T::kSmem);
   main_kernel_begin(st);
   launch_pdl(kern, dim3(prm.G), dim3(WS ? 384 : (NWM * KS * OS + 1) * 32), T::kSmem, st, xm, um,
@@ -1075,12 +1118,16 @@ void launch_t(const CUtensorMap& xm, const CUtensorMap& um, const ContractParams
 
 // Column-tile count dispatch over [NT_LO, NT_HI] (configurations whose
 // accumulators would not fit are never instantiated).
-template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT_LO, int NT_HI>
+template <bool COL, bool BATCHED, int NWM, int WM, int KS, int KD, int OS, int NT_LO, int NT_HI,
+          bool SC = false>
 void dispatch_nt(int nt, const CUtensorMap& xm, const CUtensorMap& um, const ContractParams& prm,
                  cudaStream_t st) {
   if constexpr (NT_LO <= NT_HI) {
-    if (nt == NT_LO) return launch_t<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO>(xm, um, prm, st);
-    return dispatch_nt<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO + 1, NT_HI>(nt, xm, um, prm, st);
+    if (nt == NT_LO)
+      return launch_t<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO, false, false, false, SC>(xm, um,
+                                                                                      prm, st);
+    return dispatch_nt<COL, BATCHED, NWM, WM, KS, KD, OS, NT_LO + 1, NT_HI, SC>(nt, xm, um, prm,
+                                                                              st);
   } else {
     throw InvalidError("eb_contract: unsupported column tile count");
   }
@@ -1109,6 +1156,11 @@ void dispatch_reduce(const Plan& p, int nt, const CUtensorMap& xm, const CUtenso
 void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensorMap& um,
                     const ContractParams& prm, cudaStream_t st) {
   if (p.gemm) return launch_t<false, true, 8, 16, 1, 32, 1, 8>(xm, um, prm, st);
+  if (p.batched && prm.sc.nd > 0) {  // the scatter-epilogue instantiations
+    if (p.nwm == 8) return dispatch_nt<true, true, 8, 16, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
+    if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
+    return dispatch_nt<true, true, 4, 16, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
+  }
   if (p.batched) {
     if (p.nwm == 8) return dispatch_nt<true, true, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
     if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
@@ -1118,9 +1170,12 @@ void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensor
   return dispatch_reduce<false>(p, nt, xm, um, prm, st);
 }
 
-void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStream_t st) {
+void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStream_t st,
+                  const eb_scatter* sc = nullptr) {
   check_device();
   const Plan p = plan_of(d);
+  if (sc && !(p.col && p.batched))
+    throw InvalidError("eb_contract_scatter: the scatter epilogue needs EB_COL + EB_BATCHED");
   // short contracted mode, few rows (order-5 mode 0): U resident in registers
   if (rf_run(d, ws, ws_bytes, st)) return;
   const size_t need = (p.u_bytes + p.ws_bytes);
@@ -1141,6 +1196,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   prm.R = (int)d->R;
   prm.pre = to_list(d->n_pre, d->pre);
   prm.mid = to_list(p.col ? 0 : d->n_mid, d->mid);
+  if (sc) prm.sc = *sc;
   const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
 
   // COL stages the whole factor once (pitch = R rounded up to 16, zero
@@ -1382,6 +1438,29 @@ extern "C" size_t eb_contract_workspace(const eb_contract_desc* d) {
     eb::set_error(e.what());
     return 0;
   }
+}
+
+namespace eb {
+void check_scatter(const eb_scatter* s) {
+  if (!s || s->nd < 1 || s->nd > 8 || s->n_outer < 0 || s->n_row < 0 ||
+      s->n_outer + s->n_row >= s->nd || s->n_rep < 1 || s->n_rep > 8)
+    throw InvalidError("eb_scatter: bad dims / replicas");
+  for (int d = 0; d < s->nd; ++d)
+    if (s->ext[d] < 1 || s->block[d] < 1 || s->gbase[d] < 0 ||
+        s->gbase[d] + s->ext[d] > ((int64_t)1 << 31))
+      throw InvalidError("eb_scatter: bad extent / block / base (coordinates must be < 2^31)");
+}
+}  // namespace eb
+
+extern "C" int eb_contract_scatter(const eb_contract_desc* d, const eb_scatter* s,
+                                   void* workspace, size_t workspace_bytes, void* stream) {
+  return eb::guard([&] {
+    eb::check_scatter(s);
+    if (!d) throw eb::InvalidError("eb_contract_scatter: null descriptor");
+    eb_contract_desc dd = *d;  // out is not written: any non-null placeholder passes the checks
+    if (!dd.out) dd.out = reinterpret_cast<double*>(s->dest[0]);
+    eb::run_contract(&dd, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), s);
+  });
 }
 
 extern "C" int eb_contract(const eb_contract_desc* d, void* workspace, size_t workspace_bytes,

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "einplan_b200.h"
+
 namespace eb {
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -91,6 +93,29 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// ---- scatter epilogue (eb_scatter, einplan_b200.h) ----
+// Adds the destination rank / offset contribution of dims [d0, d1) of a
+// natural-output index x (row-major over those dims); 32-bit coordinates.
+__device__ __forceinline__ void scatter_part(const eb_scatter& s, int d0, int d1, int64_t x,
+                                             int64_t& rank, int64_t& off) {
+  uint32_t r = (uint32_t)x;
+  for (int d = d1 - 1; d >= d0; --d) {
+    const uint32_t e = (uint32_t)s.ext[d];
+    const uint32_t xd = r % e;
+    r /= e;
+    const uint32_t gg = (uint32_t)s.gbase[d] + xd;
+    const uint32_t b = (uint32_t)s.block[d];
+    const uint32_t c = gg / b;
+    rank += (int64_t)c * s.rank_stride[d];
+    off += (int64_t)(gg - c * b) * s.local_stride[d];
+  }
+}
+
+__device__ __forceinline__ void scatter_store(const eb_scatter& s, int64_t rank, int64_t off,
+                                              double v) {
+  for (int k = 0; k < s.n_rep; ++k) s.dest[rank + s.rep_offset[k]][off] = v;
 }
 
 }  // namespace eb

@@ -81,6 +81,7 @@ struct Ttm2Params {
   const double* U2;
   int64_t ldu2;
   double* out;
+  eb_scatter sc;  // sc.nd > 0: scatter epilogue (the next term's blocks, not `out`)
 };
 
 template <int NW>
@@ -329,7 +330,7 @@ struct WsCfg {
   static constexpr int Smem = Stages * kXBytes + T0Slots * T0Bytes + 1024;
 };
 
-template <int JP>
+template <int JP, bool SC = false>
 __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     ttm2_ws_kernel(const __grid_constant__ CUtensorMap xmap, const Ttm2Params prm) {
   using W = WsCfg<JP>;
@@ -511,6 +512,37 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
           for (int nj = 0; nj < 2; ++nj)
             dmma884(acc[ri][mi][nj][0], acc[ri][mi][nj][1], a[ri][mi], ub[nj]);
     }
+    if constexpr (SC) {
+      // fused redistribution: out[p][r][b][c] element by element into the
+      // next term's destination blocks (outer part once per item, row part
+      // once per row, the (b, c) part per element)
+      const eb_scatter& s = prm.sc;
+      int64_t ro = 0, oo = 0;
+      scatter_part(s, 0, s.n_outer, p, ro, oo);
+#pragma unroll
+      for (int ri = 0; ri < RW; ++ri) {
+        const int64_t r = r0 + RW * w1 + ri;
+        int64_t rm = ro, om = oo;
+        if (r < prm.M) scatter_part(s, s.n_outer, s.n_outer + s.n_row, r, rm, om);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int64_t b = 8 * mi + g;
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t c = 8 * nj + 2 * l + e;
+              if (r < prm.M && b < prm.N1 && c < prm.N2) {
+                int64_t rk = rm, of = om;
+                scatter_part(s, s.n_outer + s.n_row, s.nd, b * prm.N2 + c, rk, of);
+                scatter_store(s, rk, of, acc[ri][mi][nj][e]);
+              }
+              acc[ri][mi][nj][e] = 0.0;
+            }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int ri = 0; ri < RW; ++ri) {
       const int64_t r = r0 + RW * w1 + ri;
@@ -560,19 +592,20 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
 
 template <int JP>
 void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
-  set_smem_once(ttm2_ws_kernel<JP>, WsCfg<JP>::Smem);
+  auto kern = prm.sc.nd > 0 ? ttm2_ws_kernel<JP, true> : ttm2_ws_kernel<JP, false>;
+  set_smem_once(kern, WsCfg<JP>::Smem);
   main_kernel_begin(st);
-  launch_pdl(ttm2_ws_kernel<JP>, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), WsCfg<JP>::Smem, st,
-             xmap, prm);
+  launch_pdl(kern, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), WsCfg<JP>::Smem, st, xmap, prm);
   main_kernel_end(st);
   count_launch();
 }
 
-void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
+void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st, const eb_scatter* sc = nullptr) {
   validate(d);
   check_device();
   Ttm2Params prm;
   std::memset(&prm, 0, sizeof(prm));
+  if (sc) prm.sc = *sc;
   prm.P = d->P;
   prm.Q1 = d->Q1;
   prm.Q2 = d->Q2;
@@ -595,6 +628,10 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
   const uint32_t box[4] = {16, (uint32_t)kJ, (uint32_t)kK, 1};
   const CUtensorMap xmap = make_map(d->X, 4, dims, str, box);
 #ifdef EB_AB_VARIANTS
+  if (sc) {  // the scatter epilogue lives in the warp-specialised kernels only
+    launch_ws<2>(xmap, prm, st);
+    return;
+  }
   // A/B builds only: the block-synchronous kernel with 8 / 16 consumer warps,
   // step 1 optionally pipelined (measured, C5 terms at 1965 MHz: 8 warps
   // unpipelined 1.56 ms, pipelined 1.60, 16 warps 1.73 / 2.19 —
@@ -621,6 +658,20 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st) {
 }  // namespace
 
 }  // namespace eb
+
+namespace eb {
+void check_scatter(const eb_scatter* s);
+}
+
+extern "C" int eb_ttm2_scatter(const eb_ttm2_desc* d, const eb_scatter* s, void* stream) {
+  return eb::guard([&] {
+    eb::check_scatter(s);
+    if (!d) throw eb::InvalidError("eb_ttm2_scatter: null descriptor");
+    eb_ttm2_desc dd = *d;  // out is not written
+    if (!dd.out) dd.out = s->dest[0];
+    eb::run_ttm2(&dd, static_cast<cudaStream_t>(stream), s);
+  });
+}
 
 extern "C" int eb_ttm2(const eb_ttm2_desc* d, void* stream) {
   return eb::guard([&] { eb::run_ttm2(d, static_cast<cudaStream_t>(stream)); });

@@ -894,3 +894,45 @@ def test_odd_extents_stay_on_the_dmma_path(eb, e, ext, P):
     assert st["generic_launches"] == 0, st
     assert st["fused_launches"] + st["ttm_launches"] > 0, st
     check(ex.gather(), want)
+
+
+@pytest.mark.parametrize("e,ext,P", [
+    ("ijk,jb,kc->ibc", dict(i=96, j=96, k=96, b=24, c=24), 2),    # C4-like: k2 -> i2
+    ("ijk,jb,kc->ibc", dict(i=96, j=96, k=96, b=24, c=24), 4),    # k4 -> i2 b2
+    ("ijk,jb,kc->ibc", dict(i=128, j=128, k=128, b=32, c=32), 8),
+    ("ijklm,jb,kc,ld,me->ibcde", dict(i=32, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12),
+     4),                                                            # eb_ttm2 epilogue: i2m2 -> i2c2
+])
+def test_fused_redistribution_push(eb, e, ext, P, opts):
+    """The redistribution of a TTMc intermediate fused into its producer: the
+    TTM (COL BATCHED) / TTM-pair (eb_ttm2) epilogue stores every element
+    straight into the next term's destination blocks (eb_scatter).  Bitwise
+    equal to the separate apply_plan copy, same comm accounting, and equal to
+    the oracle chain."""
+    ops = oracle.seeded_inputs(e, ext, 61)
+    if e.startswith("ijklm"):
+        want = _ttmc_o5_chain(ext, ops)
+    else:
+        want = oracle.naive_evaluate(e, ext, ops)
+    outs, stats = [], []
+    for fuse in (1, 0):
+        opts("fuse_redistribution", fuse)
+        ex = eb.Executor(e, ext, P)
+        ex.stage(ops)
+        ex.run()
+        outs.append(ex.gather())
+        stats.append(ex.stats())
+        ex.close()
+    assert stats[0]["fused_redistributions"] == 1, stats[0]
+    assert stats[1]["fused_redistributions"] == 0
+    assert stats[0]["redistribute_volume"] == stats[1]["redistribute_volume"] > 0
+    assert stats[0]["max_rank_sent"] == stats[1]["max_rank_sent"]
+    assert np.array_equal(outs[0], outs[1])
+    check(outs[0], want)
+
+
+def test_scatter_rejects_bad_descriptors(eb):
+    from paper_2206_08301_b200 import _capi as C
+    L = C.lib()
+    d = C.Ttm2Desc(1, 4, 4, 16, 4, 4, 8, 8, 4, 8, 4, 8)
+    assert L.eb_ttm2_scatter(ctypes.byref(d), None, None) == 1  # EB_E_INVALID

@@ -26,10 +26,13 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default=None, help="1MM / 2MM / 3MM")
     a = ap.parse_args()
     n = a.n
     lines = []
     for name, e in [("1MM", "ij,jk->ik"), ("2MM", "ij,jk,kl->il"), ("3MM", "ij,jk,kl,lm->im")]:
+        if a.only and name != a.only:
+            continue
         ins = e.split("->")[0].split(",")
         ext = {c: n for t in ins for c in t}
         ops = [eb.random_tensor(tuple(ext[c] for c in t), k) for k, t in enumerate(ins)]
