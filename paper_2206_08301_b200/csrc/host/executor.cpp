@@ -1175,6 +1175,7 @@ DevBlock ScheduleExecutor::run_step(const TermPlan& term, int sid, std::int64_t 
         eb_scatter sc;
         scatter_desc(term, rank, want, static_cast<int>(pos),
                      static_cast<int>(xi.size() - pos - 1), sc);
+        d.out = sc.dest[0];  // not written (the workspace query wants a non-null output)
         const std::size_t wb = eb_contract_workspace(&d);
         if (wb == 0) fail(errc::invalid_argument, "scatter TTM: no contraction plan");
         eb_ok(eb_contract_scatter(&d, &sc, workspace(wb), wb, stream_),
