@@ -276,10 +276,13 @@ __device__ __forceinline__ void emit_two(const double (&acc)[MI][NT][2],
 // BATCHED scatter epilogue: the unit (row tile mt, outer index o) stored
 // element by element into the destination blocks (eb_scatter): the outer and
 // row parts of the destination address are resolved once per unit / row,
-// the column part per element; accumulators cleared.
+// the column part comes from the CTA's shared-memory table (tab, built at
+// kernel start); column pairs go out as one 16-byte store where they stay
+// adjacent.  Accumulators cleared.
 template <int MI, int NT, int MT, int WM, bool VC>
 __device__ __forceinline__ void scatter_unit(double (&acc)[MI][NT][2], const ContractParams& prm,
-                                             int64_t mt, int64_t o, int wm, int g, int l) {
+                                             const ScatterCol* tab, int64_t mt, int64_t o, int wm,
+                                             int g, int l) {
   const eb_scatter& s = prm.sc;
   int64_t ro = 0, oo = 0;
   scatter_part(s, 0, s.n_outer, o, ro, oo);
@@ -294,13 +297,13 @@ __device__ __forceinline__ void scatter_unit(double (&acc)[MI][NT][2], const Con
       for (int j = 0; j < NT; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = VC ? 16 * (j >> 1) + 4 * l + 2 * e + (j & 1) : j * 8 + 2 * l + e;
+          if (VC && (j & 1)) continue;  // VC: (2q, 2q+1) are adjacent columns
+          if (!VC && e == 1) continue;  // non-VC: (e = 0, 1) are adjacent columns
+          const int c = VC ? 16 * (j >> 1) + 4 * l + 2 * e : j * 8 + 2 * l;
+          const double v0 = acc[i][j][e];
+          const double v1 = VC ? acc[i][j + 1][e] : acc[i][j][1];
           const int64_t gc = prm.col0 + c;
-          if (gc < prm.R) {
-            int64_t rk = rm, of = om;
-            scatter_part(s, dc, s.nd, gc, rk, of);
-            scatter_store(s, rk, of, acc[i][j][e]);
-          }
+          if (gc < prm.R) scatter_pair(s, rm, om, tab[c], tab[c + 1], gc + 1 < prm.R, v0, v1);
         }
     }
 #pragma unroll
@@ -624,6 +627,19 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
   int seg = -1;
   uint32_t it = 0;
 
+  // SC: the column part of every destination address, once per CTA
+  __shared__ ScatterCol sc_tab[SC ? NT * 8 + 1 : 1];
+  if constexpr (SC) {
+    if (threadIdx.x < NT * 8 + 1) {
+      int64_t rk = 0, of = 0;
+      const int64_t gc = prm.col0 + threadIdx.x;
+      if (gc < prm.R) scatter_part(prm.sc, prm.sc.n_outer + prm.sc.n_row, prm.sc.nd, gc, rk, of);
+      sc_tab[threadIdx.x].off = of;
+      sc_tab[threadIdx.x].rank = (int32_t)rk;
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(NCW * 32) : "memory");  // consumer warps only
+  }
+
   // TWO: the second output.  When an outer index o is complete in this CTA,
   // each warp scales its T rows by A[row] and sums them (shuffles over the 8
   // row groups of a fragment), the NWM warp sums meet in shared memory, and
@@ -764,7 +780,7 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
     }
     if constexpr (SC) {  // fused redistribution: push to the destination blocks
-      scatter_unit<MI, NT, MT, WM, VC>(acc, prm, mt, o, wm, g, l);
+      scatter_unit<MI, NT, MT, WM, VC>(acc, prm, sc_tab, mt, o, wm, g, l);
       continue;
     }
     if constexpr (BATCHED && VC) {

@@ -118,4 +118,29 @@ __device__ __forceinline__ void scatter_store(const eb_scatter& s, int64_t rank,
   for (int k = 0; k < s.n_rep; ++k) s.dest[rank + s.rep_offset[k]][off] = v;
 }
 
+// Column-part table of a scatter launch (the column dims' rank / offset
+// contributions do not depend on the item: built once per CTA in shared
+// memory, looked up per element).
+struct ScatterCol {
+  int64_t off;
+  int32_t rank;
+  int32_t pad;
+};
+
+// A pair of consecutive natural columns: one 16-byte store when both land
+// next to each other in the same destination block, else two.
+__device__ __forceinline__ void scatter_pair(const eb_scatter& s, int64_t rank, int64_t off,
+                                             const ScatterCol& c0, const ScatterCol& c1,
+                                             bool has1, double v0, double v1) {
+  const int64_t o0 = off + c0.off, o1 = off + c1.off;
+  const int64_t r0 = rank + c0.rank, r1 = rank + c1.rank;
+  if (has1 && r0 == r1 && o1 == o0 + 1 && (o0 & 1) == 0) {
+    for (int k = 0; k < s.n_rep; ++k)
+      *reinterpret_cast<double2*>(s.dest[r0 + s.rep_offset[k]] + o0) = make_double2(v0, v1);
+    return;
+  }
+  scatter_store(s, r0, o0, v0);
+  if (has1) scatter_store(s, r1, o1, v1);
+}
+
 }  // namespace eb

@@ -477,6 +477,29 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+  // SC: this lane's (b, c) parts of the destination address (the last two
+  // natural dims; fixed for the whole launch)
+  int32_t cb_rank[2] = {0, 0}, cb_off[2] = {0, 0};
+  int32_t cc_rank[2][2] = {{0, 0}, {0, 0}}, cc_off[2][2] = {{0, 0}, {0, 0}};
+  if constexpr (SC) {
+    const int nd = prm.sc.nd;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      int64_t rk = 0, of = 0;
+      if (8 * mi + g < prm.N1) scatter_part(prm.sc, nd - 2, nd - 1, 8 * mi + g, rk, of);
+      cb_rank[mi] = (int32_t)rk;
+      cb_off[mi] = (int32_t)of;
+    }
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int64_t rk = 0, of = 0;
+        if (8 * nj + 2 * l + e < prm.N2) scatter_part(prm.sc, nd - 1, nd, 8 * nj + 2 * l + e, rk, of);
+        cc_rank[nj][e] = (int32_t)rk;
+        cc_off[nj][e] = (int32_t)of;
+      }
+  }
   uint32_t it = 0;
   for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
     const int64_t p = item / prm.mtiles;
@@ -514,32 +537,37 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     }
     if constexpr (SC) {
       // fused redistribution: out[p][r][b][c] element by element into the
-      // next term's destination blocks (outer part once per item, row part
-      // once per row, the (b, c) part per element)
+      // next term's destination blocks — outer part once per item, row part
+      // once per row, the (b, c) parts from the per-lane tables built at
+      // kernel start; adjacent c pairs as one 16-byte store
       const eb_scatter& s = prm.sc;
       int64_t ro = 0, oo = 0;
       scatter_part(s, 0, s.n_outer, p, ro, oo);
 #pragma unroll
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
-        int64_t rm = ro, om = oo;
-        if (r < prm.M) scatter_part(s, s.n_outer, s.n_outer + s.n_row, r, rm, om);
+        if (r < prm.M) {
+          int64_t rm = ro, om = oo;
+          scatter_part(s, s.n_outer, s.n_outer + s.n_row, r, rm, om);
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          const int64_t b = 8 * mi + g;
+          for (int mi = 0; mi < 2; ++mi) {
+            const int64_t b = 8 * mi + g;
+            if (b >= prm.N1) continue;
 #pragma unroll
-          for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int64_t c = 8 * nj + 2 * l + e;
-              if (r < prm.M && b < prm.N1 && c < prm.N2) {
-                int64_t rk = rm, of = om;
-                scatter_part(s, s.n_outer + s.n_row, s.nd, b * prm.N2 + c, rk, of);
-                scatter_store(s, rk, of, acc[ri][mi][nj][e]);
-              }
-              acc[ri][mi][nj][e] = 0.0;
+            for (int nj = 0; nj < 2; ++nj) {
+              const int64_t c = 8 * nj + 2 * l;
+              if (c >= prm.N2) continue;
+              const ScatterCol c0 = {cc_off[nj][0] + cb_off[mi], cc_rank[nj][0] + cb_rank[mi], 0};
+              const ScatterCol c1 = {cc_off[nj][1] + cb_off[mi], cc_rank[nj][1] + cb_rank[mi], 0};
+              scatter_pair(s, rm, om, c0, c1, c + 1 < prm.N2, acc[ri][mi][nj][0],
+                           acc[ri][mi][nj][1]);
             }
+          }
         }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
       }
       continue;
     }
