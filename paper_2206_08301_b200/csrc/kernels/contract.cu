@@ -287,12 +287,14 @@ __device__ __forceinline__ void scatter_unit(double (&acc)[MI][NT][2], const Con
   int64_t ro = 0, oo = 0;
   scatter_part(s, 0, s.n_outer, o, ro, oo);
   const int dr = s.n_outer, dc = s.n_outer + s.n_row;
+  const RowBase rb = scatter_rowbase(s, dr, dc, mt * MT, MT, ro, oo);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    const int64_t row = mt * MT + wm * WM + (VC ? vc_row(i, g) : i * 8 + g);
+    const int delta = wm * WM + (VC ? vc_row(i, g) : i * 8 + g);
+    const int64_t row = mt * MT + delta;
     if (row < prm.M) {
-      int64_t rm = ro, om = oo;
-      scatter_part(s, dr, dc, row, rm, om);
+      int64_t rm, om;
+      scatter_row(s, dr, dc, rb, mt * MT, delta, ro, oo, rm, om);
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll

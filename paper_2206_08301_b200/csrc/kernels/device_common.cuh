@@ -118,6 +118,47 @@ __device__ __forceinline__ void scatter_store(const eb_scatter& s, int64_t rank,
   for (int k = 0; k < s.n_rep; ++k) s.dest[rank + s.rep_offset[k]][off] = v;
 }
 
+// Row part of the rows row0 .. row0 + span - 1 of one item: resolved once
+// at row0; when the span stays inside one run of the innermost row dim and
+// one destination block along it, row0 + delta is row0's part plus
+// delta * local_stride (no division per row).
+struct RowBase {
+  int64_t rank, off, step;
+  bool linear;
+};
+
+__device__ __forceinline__ RowBase scatter_rowbase(const eb_scatter& s, int d0, int d1,
+                                                   int64_t row0, int span, int64_t rank0,
+                                                   int64_t off0) {
+  RowBase rb{rank0, off0, 0, false};
+  if (d1 <= d0) {
+    rb.linear = true;
+    return rb;
+  }
+  const int di = d1 - 1;
+  const uint32_t e = (uint32_t)s.ext[di];
+  const uint32_t xi = (uint32_t)row0 % e;
+  const uint32_t g0 = (uint32_t)s.gbase[di] + xi;
+  const uint32_t b = (uint32_t)s.block[di];
+  rb.linear = xi + (uint32_t)span <= e && g0 / b == (g0 + (uint32_t)span - 1) / b;
+  rb.step = s.local_stride[di];
+  scatter_part(s, d0, d1, row0, rb.rank, rb.off);
+  return rb;
+}
+
+__device__ __forceinline__ void scatter_row(const eb_scatter& s, int d0, int d1, const RowBase& rb,
+                                            int64_t row0, int delta, int64_t rank0, int64_t off0,
+                                            int64_t& rank, int64_t& off) {
+  if (rb.linear) {
+    rank = rb.rank;
+    off = rb.off + (int64_t)delta * rb.step;
+    return;
+  }
+  rank = rank0;
+  off = off0;
+  scatter_part(s, d0, d1, row0 + delta, rank, off);
+}
+
 // Column-part table of a scatter launch (the column dims' rank / offset
 // contributions do not depend on the item: built once per CTA in shared
 // memory, looked up per element).

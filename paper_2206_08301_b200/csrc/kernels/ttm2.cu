@@ -543,12 +543,14 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
       const eb_scatter& s = prm.sc;
       int64_t ro = 0, oo = 0;
       scatter_part(s, 0, s.n_outer, p, ro, oo);
+      const int dr = s.n_outer, dc = s.n_outer + s.n_row;
+      const RowBase rb = scatter_rowbase(s, dr, dc, r0, kRows, ro, oo);
 #pragma unroll
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
         if (r < prm.M) {
-          int64_t rm = ro, om = oo;
-          scatter_part(s, s.n_outer, s.n_outer + s.n_row, r, rm, om);
+          int64_t rm, om;
+          scatter_row(s, dr, dc, rb, r0, RW * w1 + ri, ro, oo, rm, om);
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
             const int64_t b = 8 * mi + g;
