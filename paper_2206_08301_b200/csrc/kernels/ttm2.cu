@@ -321,11 +321,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 // j halves summed by step 1), 1 -> 4 step-0 warps each contracting all 64 j
 // (one step-0 and one step-1 warp per sub-partition, fewer non-DMMA
 // instructions per stage).
-template <int JP>
+// SC (scatter epilogue): the step-1 warps spend longer per item between
+// their t0 slices, so the t0 ring is 4 deep where shared memory allows
+// (JP = 1) and step 0 keeps streaming meanwhile.
+template <int JP, bool SC = false>
 struct WsCfg {
   static constexpr int S0 = 4 * JP, S1 = 4, Warps = S0 + S1 + 1;
   static constexpr int JW = kJ / JP, B16 = JW / 16;
-  static constexpr int Stages = 6, T0Slots = 2;
+  static constexpr int Stages = 6, T0Slots = (SC && JP == 1) ? 4 : 2;
   static constexpr int T0Bytes = JP * kK * kPlane;  // [j part][k][16 r][16 b]
   static constexpr int Smem = Stages * kXBytes + T0Slots * T0Bytes + 1024;
 };
@@ -333,7 +336,7 @@ struct WsCfg {
 template <int JP, bool SC = false>
 __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
     ttm2_ws_kernel(const __grid_constant__ CUtensorMap xmap, const Ttm2Params prm) {
-  using W = WsCfg<JP>;
+  using W = WsCfg<JP, SC>;
   constexpr int kWsS0 = W::S0, kWsS1 = W::S1, kWsStages = W::Stages, kWsT0Slots = W::T0Slots;
   constexpr int kWsT0Bytes = W::T0Bytes;
   extern __shared__ uint8_t smem_raw[];
@@ -622,10 +625,12 @@ void launch(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
 
 template <int JP>
 void launch_ws(const CUtensorMap& xmap, const Ttm2Params& prm, cudaStream_t st) {
-  auto kern = prm.sc.nd > 0 ? ttm2_ws_kernel<JP, true> : ttm2_ws_kernel<JP, false>;
-  set_smem_once(kern, WsCfg<JP>::Smem);
+  const bool sc = prm.sc.nd > 0;
+  auto kern = sc ? ttm2_ws_kernel<JP, true> : ttm2_ws_kernel<JP, false>;
+  const int smem = sc ? WsCfg<JP, true>::Smem : WsCfg<JP, false>::Smem;
+  set_smem_once(kern, smem);
   main_kernel_begin(st);
-  launch_pdl(kern, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), WsCfg<JP>::Smem, st, xmap, prm);
+  launch_pdl(kern, dim3(prm.G), dim3(WsCfg<JP>::Warps * 32), smem, st, xmap, prm);
   main_kernel_end(st);
   count_launch();
 }
