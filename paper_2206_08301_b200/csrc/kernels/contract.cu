@@ -79,6 +79,7 @@ struct ContractParams {
   // BATCHED COL: scatter epilogue (sc.nd > 0) — stores go to the next term's
   // destination blocks instead of `out`
   eb_scatter sc;
+  ScatterDiv scd;  // its dividers (launcher-made)
 };
 
 __device__ __forceinline__ double krp_value(const FacList& f, int64_t x, int col) {
@@ -285,16 +286,17 @@ __device__ __forceinline__ void scatter_unit(double (&acc)[MI][NT][2], const Con
                                              int g, int l) {
   const eb_scatter& s = prm.sc;
   int64_t ro = 0, oo = 0;
-  scatter_part(s, 0, s.n_outer, o, ro, oo);
+  const ScatterDiv& v = prm.scd;
+  scatter_part(s, v, 0, s.n_outer, o, ro, oo);
   const int dr = s.n_outer, dc = s.n_outer + s.n_row;
-  const RowBase rb = scatter_rowbase(s, dr, dc, mt * MT, MT, ro, oo);
+  const RowBase rb = scatter_rowbase(s, v, dr, dc, mt * MT, MT, ro, oo);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int delta = wm * WM + (VC ? vc_row(i, g) : i * 8 + g);
     const int64_t row = mt * MT + delta;
     if (row < prm.M) {
       int64_t rm, om;
-      scatter_row(s, dr, dc, rb, mt * MT, delta, ro, oo, rm, om);
+      scatter_row(s, v, dr, dc, rb, mt * MT, delta, ro, oo, rm, om);
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -635,7 +637,8 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
     if (threadIdx.x < NT * 8 + 1) {
       int64_t rk = 0, of = 0;
       const int64_t gc = prm.col0 + threadIdx.x;
-      if (gc < prm.R) scatter_part(prm.sc, prm.sc.n_outer + prm.sc.n_row, prm.sc.nd, gc, rk, of);
+      if (gc < prm.R)
+        scatter_part(prm.sc, prm.scd, prm.sc.n_outer + prm.sc.n_row, prm.sc.nd, gc, rk, of);
       sc_tab[threadIdx.x].off = of;
       sc_tab[threadIdx.x].rank = (int32_t)rk;
     }
@@ -1214,7 +1217,10 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   prm.R = (int)d->R;
   prm.pre = to_list(d->n_pre, d->pre);
   prm.mid = to_list(p.col ? 0 : d->n_mid, d->mid);
-  if (sc) prm.sc = *sc;
+  if (sc) {
+    prm.sc = *sc;
+    prm.scd = make_scatter_div(*sc);
+  }
   const int64_t ldu = d->ldu > 0 ? d->ldu : d->R;
 
   // COL stages the whole factor once (pitch = R rounded up to 16, zero

@@ -96,20 +96,54 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 // ---- scatter epilogue (eb_scatter, einplan_b200.h) ----
+// Division by a launch constant d < 2^31 as a multiply-high and a shift
+// (x < 2^31): q = (umulhi(x, m) + x) >> l with l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1.
+struct FastDiv {
+  uint32_t d, m;
+  int l;
+};
+
+__host__ __device__ inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.l = 0;
+  while ((1ull << f.l) < d) ++f.l;
+  f.m = (uint32_t)(((1ull << 32) * ((1ull << f.l) - d)) / d + 1);
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv& f) {
+  return (__umulhi(x, f.m) + x) >> f.l;
+}
+
+// the per-dim dividers of a scatter launch (ext and block of every dim)
+struct ScatterDiv {
+  FastDiv ext[8], block[8];
+};
+
+inline ScatterDiv make_scatter_div(const eb_scatter& s) {
+  ScatterDiv v;
+  for (int d = 0; d < 8; ++d) {
+    v.ext[d] = make_fastdiv(d < s.nd ? (uint32_t)s.ext[d] : 1u);
+    v.block[d] = make_fastdiv(d < s.nd ? (uint32_t)s.block[d] : 1u);
+  }
+  return v;
+}
+
 // Adds the destination rank / offset contribution of dims [d0, d1) of a
 // natural-output index x (row-major over those dims); 32-bit coordinates.
-__device__ __forceinline__ void scatter_part(const eb_scatter& s, int d0, int d1, int64_t x,
-                                             int64_t& rank, int64_t& off) {
+__device__ __forceinline__ void scatter_part(const eb_scatter& s, const ScatterDiv& v, int d0,
+                                             int d1, int64_t x, int64_t& rank, int64_t& off) {
   uint32_t r = (uint32_t)x;
   for (int d = d1 - 1; d >= d0; --d) {
-    const uint32_t e = (uint32_t)s.ext[d];
-    const uint32_t xd = r % e;
-    r /= e;
+    const uint32_t q = fdiv(r, v.ext[d]);
+    const uint32_t xd = r - q * v.ext[d].d;
+    r = q;
     const uint32_t gg = (uint32_t)s.gbase[d] + xd;
-    const uint32_t b = (uint32_t)s.block[d];
-    const uint32_t c = gg / b;
+    const uint32_t c = fdiv(gg, v.block[d]);
     rank += (int64_t)c * s.rank_stride[d];
-    off += (int64_t)(gg - c * b) * s.local_stride[d];
+    off += (int64_t)(gg - c * v.block[d].d) * s.local_stride[d];
   }
 }
 
@@ -127,28 +161,29 @@ struct RowBase {
   bool linear;
 };
 
-__device__ __forceinline__ RowBase scatter_rowbase(const eb_scatter& s, int d0, int d1,
-                                                   int64_t row0, int span, int64_t rank0,
-                                                   int64_t off0) {
+__device__ __forceinline__ RowBase scatter_rowbase(const eb_scatter& s, const ScatterDiv& v,
+                                                   int d0, int d1, int64_t row0, int span,
+                                                   int64_t rank0, int64_t off0) {
   RowBase rb{rank0, off0, 0, false};
   if (d1 <= d0) {
     rb.linear = true;
     return rb;
   }
   const int di = d1 - 1;
-  const uint32_t e = (uint32_t)s.ext[di];
-  const uint32_t xi = (uint32_t)row0 % e;
+  const uint32_t e = v.ext[di].d;
+  const uint32_t xi = (uint32_t)row0 - fdiv((uint32_t)row0, v.ext[di]) * e;
   const uint32_t g0 = (uint32_t)s.gbase[di] + xi;
-  const uint32_t b = (uint32_t)s.block[di];
-  rb.linear = xi + (uint32_t)span <= e && g0 / b == (g0 + (uint32_t)span - 1) / b;
+  rb.linear = xi + (uint32_t)span <= e &&
+              fdiv(g0, v.block[di]) == fdiv(g0 + (uint32_t)span - 1, v.block[di]);
   rb.step = s.local_stride[di];
-  scatter_part(s, d0, d1, row0, rb.rank, rb.off);
+  scatter_part(s, v, d0, d1, row0, rb.rank, rb.off);
   return rb;
 }
 
-__device__ __forceinline__ void scatter_row(const eb_scatter& s, int d0, int d1, const RowBase& rb,
-                                            int64_t row0, int delta, int64_t rank0, int64_t off0,
-                                            int64_t& rank, int64_t& off) {
+__device__ __forceinline__ void scatter_row(const eb_scatter& s, const ScatterDiv& v, int d0,
+                                            int d1, const RowBase& rb, int64_t row0, int delta,
+                                            int64_t rank0, int64_t off0, int64_t& rank,
+                                            int64_t& off) {
   if (rb.linear) {
     rank = rb.rank;
     off = rb.off + (int64_t)delta * rb.step;
@@ -156,7 +191,7 @@ __device__ __forceinline__ void scatter_row(const eb_scatter& s, int d0, int d1,
   }
   rank = rank0;
   off = off0;
-  scatter_part(s, d0, d1, row0 + delta, rank, off);
+  scatter_part(s, v, d0, d1, row0 + delta, rank, off);
 }
 
 // Column-part table of a scatter launch (the column dims' rank / offset

@@ -82,6 +82,7 @@ struct Ttm2Params {
   int64_t ldu2;
   double* out;
   eb_scatter sc;  // sc.nd > 0: scatter epilogue (the next term's blocks, not `out`)
+  ScatterDiv scd;
 };
 
 template <int NW>
@@ -489,7 +490,7 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
       int64_t rk = 0, of = 0;
-      if (8 * mi + g < prm.N1) scatter_part(prm.sc, nd - 2, nd - 1, 8 * mi + g, rk, of);
+      if (8 * mi + g < prm.N1) scatter_part(prm.sc, prm.scd, nd - 2, nd - 1, 8 * mi + g, rk, of);
       cb_rank[mi] = (int32_t)rk;
       cb_off[mi] = (int32_t)of;
     }
@@ -498,7 +499,8 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         int64_t rk = 0, of = 0;
-        if (8 * nj + 2 * l + e < prm.N2) scatter_part(prm.sc, nd - 1, nd, 8 * nj + 2 * l + e, rk, of);
+        if (8 * nj + 2 * l + e < prm.N2)
+          scatter_part(prm.sc, prm.scd, nd - 1, nd, 8 * nj + 2 * l + e, rk, of);
         cc_rank[nj][e] = (int32_t)rk;
         cc_off[nj][e] = (int32_t)of;
       }
@@ -545,15 +547,16 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
       // kernel start; adjacent c pairs as one 16-byte store
       const eb_scatter& s = prm.sc;
       int64_t ro = 0, oo = 0;
-      scatter_part(s, 0, s.n_outer, p, ro, oo);
+      const ScatterDiv& v = prm.scd;
+      scatter_part(s, v, 0, s.n_outer, p, ro, oo);
       const int dr = s.n_outer, dc = s.n_outer + s.n_row;
-      const RowBase rb = scatter_rowbase(s, dr, dc, r0, kRows, ro, oo);
+      const RowBase rb = scatter_rowbase(s, v, dr, dc, r0, kRows, ro, oo);
 #pragma unroll
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
         if (r < prm.M) {
           int64_t rm, om;
-          scatter_row(s, dr, dc, rb, r0, RW * w1 + ri, ro, oo, rm, om);
+          scatter_row(s, v, dr, dc, rb, r0, RW * w1 + ri, ro, oo, rm, om);
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
             const int64_t b = 8 * mi + g;
@@ -640,7 +643,10 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st, const eb_scatter* sc = nul
   check_device();
   Ttm2Params prm;
   std::memset(&prm, 0, sizeof(prm));
-  if (sc) prm.sc = *sc;
+  if (sc) {
+    prm.sc = *sc;
+    prm.scd = make_scatter_div(*sc);
+  }
   prm.P = d->P;
   prm.Q1 = d->Q1;
   prm.Q2 = d->Q2;
