@@ -140,6 +140,18 @@ typedef struct eb_ttm2_desc {
 
 int eb_ttm2(const eb_ttm2_desc* d, void* stream);
 
+/* Both terms of the TTMc-O5 schedule ([t0,t1], [t2,out]) in ONE persistent
+ * launch when the t1 hand-over between them is a whole-block self message
+ * (the reference's apply_plan copy, redistribute.cpp:185-206; C5 at P = 1,
+ * 2, 8): term A (a: X -> a->out = t1) and term B (b: b->X == a->out, viewed
+ * as [P][Q1b][Q2b][Mb] with Q1b Q2b Mb = Ma N1a N2a -> b->out).  t1 passes
+ * through L2 (evict-last stores, discarded once read) instead of HBM; term B
+ * of slab p starts once every term-A tile of p is stored (in-kernel counters,
+ * workspace = eb_ttm2_chain_workspace(a) bytes, zeroed by the call). */
+size_t eb_ttm2_chain_workspace(const eb_ttm2_desc* a);
+int eb_ttm2_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
 /* eb_contract (EB_COL, EB_BATCHED only) / eb_ttm2 with the scatter epilogue;
  * d->out is ignored. */
 int eb_contract_scatter(const eb_contract_desc* d, const eb_scatter* s, void* workspace,
@@ -226,7 +238,8 @@ int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fas
  * "gemm" 0 auto / 1 forced / 2 off (wide GEMM steps: one launch over
  * (row tile, 64-column block) items instead of per-64-column split-K),
  * "fuse_redistribution" 0/1 (TTM outputs pushed by the producing kernel into
- * the next term's blocks, eb_scatter). */
+ * the next term's blocks, eb_scatter), "chain_terms" 0/1 (two TTM-pair
+ * terms joined by a self hand-over in one eb_ttm2_chain launch). */
 int eb_set_option(const char* name, const char* value);
 
 /* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------

@@ -996,6 +996,79 @@ bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
   return true;
 }
 
+const TermPlan* ScheduleExecutor::chain_next(const TermPlan& a) const {
+  if (!eb::options().fuse_ttm2 || !eb::options().chain_terms || a.reduction.depth > 1)
+    return nullptr;
+  const TermPlan* b = nullptr;
+  for (const TermPlan& t : pipe_.schedule.terms)
+    if (t.index == a.index + 1) b = &t;
+  if (!b || b->reduction.depth > 1) return nullptr;
+  const RedistRecord* rec = find_redist(b->index, a.statement.output);
+  if (!rec) return nullptr;
+  // every rank's t1 block is the same block in both terms: whole self messages
+  const TensorPlacement& sp = rec->plan.source;
+  const TensorPlacement& dp = rec->plan.destination;
+  if (sp.dist.blocks != dp.dist.blocks || sp.dist.extents != dp.dist.extents) return nullptr;
+  for (std::int64_t r = 0; r < pipe_.schedule.procs; ++r)
+    if (sp.block_coords_of(r) != dp.block_coords_of(r)) return nullptr;
+  for (const Message& m : rec->plan.messages)
+    if (!m.self) return nullptr;
+  eb_ttm2_desc da, db;
+  std::string na, nb;
+  int p0 = 0, r0 = 0;
+  for (std::int64_t r : owned_) {
+    if (!ttm2_shape(a, r, da, na, p0, r0) || !ttm2_shape(*b, r, db, nb, p0, r0)) return nullptr;
+    const ContractionStep& b0 = pipe_.tree.steps[static_cast<std::size_t>(b->step_ids[0])];
+    if (b0.lhs_indices != na || pipe_.tree.tensor_name(b0.lhs) != a.statement.output)
+      return nullptr;
+    if (da.P != db.P || db.Q1 * db.Q2 * db.M != da.M * da.N1 * da.N2) return nullptr;
+  }
+  return b;
+}
+
+void ScheduleExecutor::run_chain(const TermPlan& a, const TermPlan& b, std::int64_t rank,
+                                 const std::map<std::string, const DevBlock*>& at_hand,
+                                 DevBlock& t1, DevBlock& out) {
+  eb_ttm2_desc da, db;
+  std::string na, nb;
+  int np = 0, nr = 0;
+  ttm2_shape(a, rank, da, na, np, nr);
+  ttm2_shape(b, rank, db, nb, np, nr);
+  const ContractionTree& tree = pipe_.tree;
+  const ContractionStep& a0 = tree.steps[static_cast<std::size_t>(a.step_ids[0])];
+  const ContractionStep& a1 = tree.steps[static_cast<std::size_t>(a.step_ids[1])];
+  const ContractionStep& b0 = tree.steps[static_cast<std::size_t>(b.step_ids[0])];
+  const ContractionStep& b1 = tree.steps[static_cast<std::size_t>(b.step_ids[1])];
+  auto input = [&](const TermPlan& t, int id) -> const DevBlock& {
+    const std::string name = tree.tensor_name(id);
+    const auto it = at_hand.find(name);
+    if (it != at_hand.end()) return *it->second;
+    return inputs_.at({t.index, name})[static_cast<std::size_t>(rank)];
+  };
+  const DevBlock& x = input(a, a0.lhs);
+  const DevBlock& u1 = input(a, a0.rhs);
+  const DevBlock& u2 = input(a, a1.rhs);
+  const DevBlock& u3 = input(b, b0.rhs);
+  const DevBlock& u4 = input(b, b1.rhs);
+  t1 = new_block(a, na, rank, false, true);
+  out = new_block(b, nb, rank, false, true);
+  da.X = x.ptr;
+  da.U1 = u1.ptr;
+  da.ldu1 = u1.shape[1];
+  da.U2 = u2.ptr;
+  da.ldu2 = u2.shape[1];
+  da.out = t1.ptr;
+  db.X = t1.ptr;
+  db.U1 = u3.ptr;
+  db.ldu1 = u3.shape[1];
+  db.U2 = u4.ptr;
+  db.ldu2 = u4.shape[1];
+  db.out = out.ptr;
+  const std::size_t wb = eb_ttm2_chain_workspace(&da);
+  eb_ok(eb_ttm2_chain(&da, &db, workspace(wb), wb, stream_), "eb_ttm2_chain (both TTMc terms)");
+  ++launches_fused_;
+}
+
 namespace {
 bool uniform_blocks(const TensorPlacement& pl) {
   for (std::size_t d = 0; d < pl.indices.size(); ++d) {
@@ -1009,6 +1082,7 @@ bool uniform_blocks(const TensorPlacement& pl) {
 
 const RedistRecord* ScheduleExecutor::push_record(const TermPlan& t) const {
   if (!eb::options().fuse_redistribution || t.reduction.depth > 1) return nullptr;
+  if (chain_next(t)) return nullptr;  // the two terms run as one chained launch
   // the producer stores into every destination block: all of them must be
   // addressable here (one device, or the peers' mapped heaps — not NCCL)
   if (!transport_->is_virtual() && !transport_->peer_mapped()) return nullptr;
@@ -1291,6 +1365,7 @@ void ScheduleExecutor::execute() {
   redistributions_fused_ = 0;
   const std::int64_t procs = pipe_.schedule.procs;
   pushed_.clear();
+  chain_out_.clear();
   push_rec_ = nullptr;
   prepare_heap();
 
@@ -1374,10 +1449,22 @@ void ScheduleExecutor::execute() {
     std::vector<DevBlock> out_blocks(static_cast<std::size_t>(procs));
     push_rec_ = push_record(term);
     if (push_rec_) arm_push();
+    const TermPlan* chained = chain_next(term);
     for (std::int64_t rank : owned_) {
       std::map<std::string, const DevBlock*> at_hand;
       for (auto& kv : arrays) at_hand[kv.first] = &(*kv.second)[static_cast<std::size_t>(rank)];
+      if (chain_out_.count({term.index, rank})) {  // computed with the previous term
+        out_blocks[static_cast<std::size_t>(rank)] = chain_out_.at({term.index, rank});
+        continue;
+      }
       DevBlock result;
+      if (chained) {
+        DevBlock out_next;
+        run_chain(term, *chained, rank, at_hand, result, out_next);
+        out_blocks[static_cast<std::size_t>(rank)] = result;
+        chain_out_[{chained->index, rank}] = out_next;
+        continue;
+      }
       if (try_fused_mttkrp(term, rank, at_hand, result) ||
           (eb::options().fuse_ttm2 && try_fused_ttm2(term, rank, at_hand, result))) {
         out_blocks[static_cast<std::size_t>(rank)] = result;

@@ -234,6 +234,13 @@ class ScheduleExecutor {
   // else nullptr.  A function of the schedule only: every rank agrees.
   const RedistRecord* push_record(const TermPlan& t) const;
   void arm_push();  // destination blocks of every rank (push_dst_)
+  // Term chaining: the next term when both are TTM pairs joined by a
+  // whole-block self hand-over of the intermediate (eb_ttm2_chain), else
+  // nullptr; run_chain launches both for one rank.
+  const TermPlan* chain_next(const TermPlan& a) const;
+  void run_chain(const TermPlan& a, const TermPlan& b, std::int64_t rank,
+                 const std::map<std::string, const DevBlock*>& at_hand, DevBlock& t1,
+                 DevBlock& out);
   void scatter_desc(const TermPlan& term, std::int64_t rank, const std::string& natural,
                     int n_outer, int n_row, eb_scatter& sc) const;
   bool try_fused_mttkrp(const TermPlan& term, std::int64_t rank,
@@ -276,6 +283,7 @@ class ScheduleExecutor {
   const RedistRecord* push_rec_ = nullptr;
   std::vector<DevBlock> push_dst_;
   std::set<std::pair<int, std::string>> pushed_;
+  std::map<std::pair<int, std::int64_t>, DevBlock> chain_out_;  // (term, rank) -> output
 };
 
 }  // namespace gpu

@@ -44,6 +44,7 @@ Options read_env() {
   if (const char* v = std::getenv("EB_FUSE_TTM2")) o.fuse_ttm2 = v[0] != '0';
   if (const char* v = std::getenv("EB_GEMM")) o.gemm = std::atoi(v);
   if (const char* v = std::getenv("EB_FUSE_REDIST")) o.fuse_redistribution = v[0] != '0';
+  if (const char* v = std::getenv("EB_CHAIN_TERMS")) o.chain_terms = v[0] != '0';
   return o;
 }
 
@@ -109,6 +110,8 @@ extern "C" int eb_set_option(const char* name, const char* value) {
       o.ttm2_variant = v;
     } else if (!std::strcmp(name, "fuse_ttm2")) {
       o.fuse_ttm2 = v != 0;
+    } else if (!std::strcmp(name, "chain_terms")) {
+      o.chain_terms = v != 0;
     } else if (!std::strcmp(name, "fuse_redistribution")) {
       o.fuse_redistribution = v != 0;
     } else if (!std::strcmp(name, "gemm")) {

@@ -70,6 +70,7 @@ struct Options {
   int fuse_ttm2 = 1;      // executor: TTM pairs on eb_ttm2 (0: two eb_contract launches)
   int gemm = 0;           // wide GEMM steps: 0 auto, 1 GEMM mode forced, 2 split-K chunks
   int fuse_redistribution = 1;  // executor: push TTM outputs into the next term's blocks
+  int chain_terms = 1;    // executor: chained TTM-pair terms in one launch (eb_ttm2_chain)
 };
 const Options& options();
 

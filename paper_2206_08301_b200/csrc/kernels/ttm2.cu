@@ -696,6 +696,412 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st, const eb_scatter* sc = nul
     launch_ws<2>(xmap, prm, st);
 }
 
+// ===================================================================
+// Chained TTM pairs: the two terms of the TTMc-O5 schedule in ONE persistent
+// launch, the intermediate t1 handed from term A to term B through L2.
+//
+//   A: t1[p][r][b][c]  = sum_{j,k} X [p][j][k][r] U1a[j][b] U2a[k][c]
+//   B: out[p][s][d][e] = sum_{l,m} t1[p][l][m][s] U1b[l][d] U2b[m][e]
+//      (t1 viewed as [P][Q1b][Q2b][Mb]: r = (l, m), s = (b, c))
+//
+// Used when the t1 "redistribution" between the terms is a whole-block self
+// message on every rank (C5 at P = 1, 2, 8): the reference copies the block
+// (apply_plan), the two-launch path writes 537 MB of t1 to HBM and reads it
+// back; here t1 is written with an L2 evict-last hint, read by term B while
+// still L2-resident, and its lines are discarded from L2 once read, so it
+// never costs HBM bandwidth.  X streams with an evict-first hint.
+//
+// Item order: groups g = 0..P, group g = [A(g) tiles][B(g-1) tiles] (B of a
+// slab one slab behind its A); items dealt round-robin to the CTAs, so every
+// dependency (B(p) on all A(p) tiles) points to lower item indices and every
+// CTA is resident (one per SM): progress is guaranteed.  The producer waits
+// for done[p] = #A(p) tiles (acquire, bounded: traps after ~4 s instead of
+// hanging) before the first TMA read of t1[p]; the step-1 warps release
+// done[p] after an A tile's stores.
+// ===================================================================
+
+struct ChainTerm {
+  int64_t Q1, Q2, M, N1, N2, mtiles, KC;
+  const double* U1;
+  int64_t ldu1;
+  const double* U2;
+  int64_t ldu2;
+  double* out;
+};
+
+struct ChainParams {
+  int64_t P, groups, gsize, items;  // gsize = A.mtiles + B.mtiles
+  int G;
+  ChainTerm t[2];
+  unsigned* done;  // [P] completed A tiles per slab (zeroed before launch)
+};
+
+constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
+
+__device__ __forceinline__ void tma_load_4d_hint(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1, int c2, int c3, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar),
+      "l"(hint)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_hint_v2(double* p, double a, double b, uint64_t hint) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b),
+               "l"(hint)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_hint_f64(double* p, double a, uint64_t hint) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a), "l"(hint) : "memory");
+}
+
+// item -> (term, slab p, row tile); term -1 = empty slot (group 0's B part,
+// group P's A part)
+__device__ __forceinline__ int chain_item(const ChainParams& c, int64_t item, int64_t& p,
+                                          int64_t& tile) {
+  const int64_t gi = item / c.gsize, r = item - gi * c.gsize;
+  if (r < c.t[0].mtiles) {
+    p = gi;
+    tile = r;
+    return gi < c.P ? 0 : -1;
+  }
+  p = gi - 1;
+  tile = r - c.t[0].mtiles;
+  return gi >= 1 ? 1 : -1;
+}
+
+__global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
+    ttm2_chain_kernel(const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ CUtensorMap tmap, const ChainParams prm) {
+  using W = WsCfg<1, true>;  // JP = 1, 4-deep t0 ring
+  constexpr int kS0 = W::S0, kS1 = W::S1, kStages = W::Stages, kT0Slots = W::T0Slots;
+  constexpr int kT0Bytes = W::T0Bytes;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_x[kStages];
+  __shared__ __align__(8) uint64_t empty_x[kStages];
+  __shared__ __align__(8) uint64_t full_t[kT0Slots];
+  __shared__ __align__(8) uint64_t empty_t[kT0Slots];
+
+  const uint32_t raw = smem_addr(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const sbase = smem_raw + (base - raw);
+  uint8_t* const t0s = sbase + kStages * kXBytes;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, l = lane & 3;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_addr(&full_x[s]), 1);
+      mbar_init(smem_addr(&empty_x[s]), kS0);
+    }
+    for (int s = 0; s < kT0Slots; ++s) {
+      mbar_init(smem_addr(&full_t[s]), kS0);
+      mbar_init(smem_addr(&empty_t[s]), kS1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == kS0 + kS1) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      tma_prefetch_desc(&xmap);
+      tma_prefetch_desc(&tmap);
+      uint32_t it = 0;
+      int64_t ready = -1;  // highest slab whose t1 this CTA has seen complete
+      for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+        int64_t p, tile;
+        const int tt = chain_item(prm, item, p, tile);
+        if (tt < 0) continue;
+        const ChainTerm& T = prm.t[tt];
+        if (tt == 1 && p > ready) {
+          // every A tile of slab p stored (acquire), then order the async
+          // proxy (TMA) after it
+          const unsigned want = (unsigned)prm.t[0].mtiles;
+          long long spins = 0;
+          for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(prm.done + p) : "memory");
+            if (v >= want) break;
+            __nanosleep(64);
+            if (++spins > (1ll << 26)) __trap();  // ~4 s: a broken dependency, not a hang
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          ready = p;
+        }
+        const int r0 = (int)(tile * kRows);
+        for (int64_t kc = 0; kc < T.KC; ++kc, ++it) {
+          const int st = it % kStages;
+          if (it >= (uint32_t)kStages)
+            mbar_wait(smem_addr(&empty_x[st]), ((it / kStages) - 1) & 1);
+          const uint32_t fb = smem_addr(&full_x[st]);
+          mbar_expect_tx(fb, kXBytes);
+          if (tt == 0)
+            tma_load_4d_hint(base + st * kXBytes, &xmap, fb, r0, 0, (int)(kc * kK), (int)p,
+                             kEvictFirst);
+          else
+            tma_load_4d_hint(base + st * kXBytes, &tmap, fb, r0, 0, (int)(kc * kK), (int)p,
+                             kEvictFirst);
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp < kS0) {
+    // ------------------------------------------------------------- step 0
+    const int kk = warp;  // JP = 1: warp kk contracts all 64 j for k = 4 kc + kk
+    double u1[W::B16][4][2];
+    int cur = -1;
+    uint32_t offa[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int j = 2 * l + (s & 1) + 8 * (s >> 1);
+      offa[s] = (uint32_t)(kk * kJ + j) * 128u + (uint32_t)(g ^ (j & 7)) * 16u;
+    }
+    uint32_t offw[2][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int r = 2 * g + mi;
+        const uint32_t chunk = (uint32_t)((4 * nj + l) ^ (4 * ((r >> 1) & 1)) ^ (2 * kk));
+        offw[mi][nj] = (uint32_t)kk * kPlane + (uint32_t)r * 128u + chunk * 16u;
+      }
+    uint32_t it = 0;
+    for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+      int64_t p, tile;
+      const int tt = chain_item(prm, item, p, tile);
+      if (tt < 0) continue;
+      const ChainTerm& T = prm.t[tt];
+      if (tt != cur) {  // this term's U1 into registers
+#pragma unroll
+        for (int b16 = 0; b16 < W::B16; ++b16)
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int nj = 0; nj < 2; ++nj) {
+              const int64_t j = 16 * b16 + 2 * l + (s & 1) + 8 * (s >> 1);
+              const int64_t n = 8 * nj + g;
+              u1[b16][s][nj] = (j < T.Q1 && n < T.N1) ? __ldg(T.U1 + j * T.ldu1 + n) : 0.0;
+            }
+        cur = tt;
+      }
+      for (int64_t kc = 0; kc < T.KC; ++kc, ++it) {
+        const int st = it % kStages;
+        mbar_wait(smem_addr(&full_x[st]), (it / kStages) & 1);
+        const uint8_t* xs = sbase + st * kXBytes;
+        double t[2][2][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) t[mi][nj][0] = t[mi][nj][1] = 0.0;
+#pragma unroll
+        for (int b16 = 0; b16 < W::B16; ++b16)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const double2 a2 = *reinterpret_cast<const double2*>(xs + offa[s] + b16 * 16 * 128);
+#pragma unroll
+            for (int nj = 0; nj < 2; ++nj) {
+              dmma884(t[0][nj][0], t[0][nj][1], a2.x, u1[b16][s][nj]);
+              dmma884(t[1][nj][0], t[1][nj][1], a2.y, u1[b16][s][nj]);
+            }
+          }
+        if (tt == 1) {
+          // t1 lines of this stage are consumed (they sit in shared memory):
+          // drop them from L2 without a write-back.  Box lines (j, kk) of
+          // t1[p][j][4 kc + kk][r0 .. r0 + 15]; lane covers j = lane, lane + 32.
+          const int64_t k = kc * kK + kk;
+          if (k < T.Q2) {
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int64_t j = lane + 32 * jj;
+              if (j < T.Q1) {
+                const double* line =
+                    prm.t[0].out + ((p * T.Q1 + j) * T.Q2 + k) * T.M + tile * kRows;
+                if (tile * kRows + kRows <= T.M && ((reinterpret_cast<uintptr_t>(line) & 127) == 0))
+                  asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&empty_x[st]));
+        const int ts = it % kT0Slots;
+        if (it >= (uint32_t)kT0Slots) mbar_wait(smem_addr(&empty_t[ts]), ((it / kT0Slots) - 1) & 1);
+        uint8_t* tb = t0s + ts * kT0Bytes;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+            *reinterpret_cast<double2*>(tb + offw[mi][nj]) = make_double2(t[mi][nj][0], t[mi][nj][1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_addr(&full_t[ts]));
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- step 1
+  const int w1 = warp - kS0;
+  constexpr int RW = kRows / kS1;
+  uint32_t offr[RW][2];
+#pragma unroll
+  for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = RW * w1 + ri;
+      const uint32_t chunk = (uint32_t)((4 * mi + (g >> 1)) ^ (4 * ((r >> 1) & 1)) ^ (2 * l));
+      offr[ri][mi] = (uint32_t)l * kPlane + (uint32_t)r * 128u + chunk * 16u + (g & 1) * 8u;
+    }
+  double acc[RW][2][2][2];
+#pragma unroll
+  for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+  uint32_t it = 0;
+  for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+    int64_t p, tile;
+    const int tt = chain_item(prm, item, p, tile);
+    if (tt < 0) continue;
+    const ChainTerm& T = prm.t[tt];
+    const int64_t r0 = tile * kRows;
+    for (int64_t kc = 0; kc < T.KC; ++kc, ++it) {
+      double ub[2];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const int64_t k = kc * kK + l, c = 8 * nj + g;
+        ub[nj] = (k < T.Q2 && c < T.N2) ? __ldg(T.U2 + k * T.ldu2 + c) : 0.0;
+      }
+      const int ts = it % kT0Slots;
+      mbar_wait(smem_addr(&full_t[ts]), (it / kT0Slots) & 1);
+      const uint8_t* tb = t0s + ts * kT0Bytes;
+      double a[RW][2];
+#pragma unroll
+      for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) a[ri][mi] = *reinterpret_cast<const double*>(tb + offr[ri][mi]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty_t[ts]));
+#pragma unroll
+      for (int ri = 0; ri < RW; ++ri)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+            dmma884(acc[ri][mi][nj][0], acc[ri][mi][nj][1], a[ri][mi], ub[nj]);
+    }
+    // out[p][r][b][c]: A -> t1 (evict-last: term B reads it from L2),
+    // B -> the final output
+    const uint64_t hint = tt == 0 ? kEvictLast : kEvictFirst;
+#pragma unroll
+    for (int ri = 0; ri < RW; ++ri) {
+      const int64_t r = r0 + RW * w1 + ri;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int64_t b = 8 * mi + g;
+        if (r < T.M && b < T.N1) {
+          double* dst = T.out + ((p * T.M + r) * T.N1 + b) * T.N2;
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) {
+            const int64_t c = 8 * nj + 2 * l;
+            if (c + 1 < T.N2 && (reinterpret_cast<uintptr_t>(dst + c) & 15) == 0) {
+              st_hint_v2(dst + c, acc[ri][mi][nj][0], acc[ri][mi][nj][1], hint);
+            } else {
+              if (c < T.N2) st_hint_f64(dst + c, acc[ri][mi][nj][0], hint);
+              if (c + 1 < T.N2) st_hint_f64(dst + c + 1, acc[ri][mi][nj][1], hint);
+            }
+          }
+        }
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+      }
+    }
+    if (tt == 0) {
+      // release this A tile of slab p once all four step-1 warps stored it
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("bar.sync 3, %0;" ::"n"(kS1 * 32) : "memory");
+      if (w1 == 0 && lane == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(prm.done + p) : "memory");
+      }
+    }
+  }
+}
+
+void validate_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b) {
+  validate(a);
+  validate(b);
+  if (a->P != b->P) throw InvalidError("eb_ttm2_chain: the two terms must share P");
+  if (b->Q1 * b->Q2 * b->M != a->M * a->N1 * a->N2)
+    throw InvalidError("eb_ttm2_chain: term B's input must be term A's output block");
+  if (b->X != a->out) throw InvalidError("eb_ttm2_chain: term B must read term A's output");
+  if (a->P > (1ll << 30) || a->M * a->N1 * a->N2 % 2 != 0)
+    throw InvalidError("eb_ttm2_chain: unsupported extents");
+}
+
+ChainTerm chain_term(const eb_ttm2_desc* d) {
+  ChainTerm t;
+  t.Q1 = d->Q1;
+  t.Q2 = d->Q2;
+  t.M = d->M;
+  t.N1 = d->N1;
+  t.N2 = d->N2;
+  t.mtiles = (d->M + kRows - 1) / kRows;
+  t.KC = (d->Q2 + kK - 1) / kK;
+  t.U1 = d->U1;
+  t.ldu1 = d->ldu1;
+  t.U2 = d->U2;
+  t.ldu2 = d->ldu2;
+  t.out = d->out;
+  return t;
+}
+
+CUtensorMap ttm2_xmap(const double* X, const eb_ttm2_desc* d) {
+  const uint64_t dims[4] = {(uint64_t)d->M, (uint64_t)d->Q1, (uint64_t)d->Q2, (uint64_t)d->P};
+  const uint64_t str[3] = {(uint64_t)(d->Q2 * d->M) * 8, (uint64_t)d->M * 8,
+                           (uint64_t)(d->Q1 * d->Q2 * d->M) * 8};
+  const uint32_t box[4] = {16, (uint32_t)kJ, (uint32_t)kK, 1};
+  return make_map(X, 4, dims, str, box);
+}
+
+void run_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
+  validate_chain(a, b);
+  check_device();
+  if (ws_bytes < (size_t)a->P * sizeof(unsigned) || !ws)
+    throw InvalidError("eb_ttm2_chain: workspace too small");
+  ChainParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.P = a->P;
+  prm.t[0] = chain_term(a);
+  prm.t[1] = chain_term(b);
+  prm.gsize = prm.t[0].mtiles + prm.t[1].mtiles;
+  prm.groups = a->P + 1;
+  prm.items = prm.groups * prm.gsize;
+  prm.G = sm_count();
+  prm.done = static_cast<unsigned*>(ws);
+  EB_CUDA(cudaMemsetAsync(ws, 0, (size_t)a->P * sizeof(unsigned), st));
+  const CUtensorMap xmap = ttm2_xmap(a->X, a);
+  const CUtensorMap tmap = ttm2_xmap(b->X, b);
+  using W = WsCfg<1, true>;
+  set_smem_once(ttm2_chain_kernel, W::Smem);
+  main_kernel_begin(st);
+  // a plain launch (no PDL): every CTA must be able to become resident for
+  // the in-kernel slab dependencies
+  ttm2_chain_kernel<<<prm.G, W::Warps * 32, W::Smem, st>>>(xmap, tmap, prm);
+  EB_CUDA(cudaGetLastError());
+  main_kernel_end(st);
+  count_launch();
+}
+
 }  // namespace
 
 }  // namespace eb
@@ -711,6 +1117,18 @@ extern "C" int eb_ttm2_scatter(const eb_ttm2_desc* d, const eb_scatter* s, void*
     eb_ttm2_desc dd = *d;  // out is not written
     if (!dd.out) dd.out = s->dest[0];
     eb::run_ttm2(&dd, static_cast<cudaStream_t>(stream), s);
+  });
+}
+
+extern "C" size_t eb_ttm2_chain_workspace(const eb_ttm2_desc* a) {
+  return a ? ((size_t)a->P * sizeof(unsigned) + 255) / 256 * 256 : 0;
+}
+
+extern "C" int eb_ttm2_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  return eb::guard([&] {
+    if (!a || !b) throw eb::InvalidError("eb_ttm2_chain: null descriptor");
+    eb::run_chain(a, b, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -173,8 +173,19 @@ def test_ttmc_o5_fused_terms(eb, P, opts):
     ex.stage(ops)
     ex.run()
     st = ex.stats()
-    assert st["fused_launches"] == 2 * P and st["ttm_launches"] == 0, st
+    # the two terms chain into one eb_ttm2_chain launch per rank where the t1
+    # hand-over is a whole-block self message (P = 1, 2, 8 here), else two
+    plan_r = json.loads(eb.plan_json(e, ext, P, include_messages=True))
+    selfonly = all(m["self"] for r in plan_r["schedule"]["redistributions"]
+                   for m in r["plan"]["messages"])
+    assert st["fused_launches"] == (P if selfonly else 2 * P) and st["ttm_launches"] == 0, st
     assert st["generic_launches"] == 0, st
+    check(ex.gather(), want)
+    opts("chain_terms", 0)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    ex.run()
+    assert ex.stats()["fused_launches"] == 2 * P
     check(ex.gather(), want)
     opts("fuse_ttm2", 0)
     ex = eb.Executor(e, ext, P)
@@ -936,3 +947,31 @@ def test_scatter_rejects_bad_descriptors(eb):
     L = C.lib()
     d = C.Ttm2Desc(1, 4, 4, 16, 4, 4, 8, 8, 4, 8, 4, 8)
     assert L.eb_ttm2_scatter(ctypes.byref(d), None, None) == 1  # EB_E_INVALID
+
+
+@pytest.mark.parametrize("P,ext", [
+    (1, dict(i=32, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12)),
+    (2, dict(i=64, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12)),
+    (1, dict(i=20, j=24, k=20, l=18, m=14, b=16, c=16, d=16, e=16)),   # ragged row tiles
+    (2, dict(i=128, j=32, k=32, l=32, m=32, b=16, c=16, d=16, e=16)),
+])
+def test_ttm2_chain_both_terms_one_launch(eb, P, ext, opts):
+    """TTMc-O5 with both terms in one persistent eb_ttm2_chain launch per rank
+    (t1 handed over through L2, slab dependencies inside the grid): equal to
+    the oracle chain and to the two-launch path, repeatedly (the in-kernel
+    counters are re-zeroed per launch)."""
+    e = "ijklm,jb,kc,ld,me->ibcde"
+    ops = oracle.seeded_inputs(e, ext, 71)
+    want = _ttmc_o5_chain(ext, ops)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    for _ in range(3):
+        ex.run()
+        assert ex.stats()["fused_launches"] == P
+        check(ex.gather(), want)
+    opts("chain_terms", 0)
+    ex2 = eb.Executor(e, ext, P)
+    ex2.stage(ops)
+    ex2.run()
+    assert ex2.stats()["fused_launches"] == 2 * P
+    check(ex2.gather(), want)
