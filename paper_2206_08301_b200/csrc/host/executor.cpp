@@ -1093,6 +1093,13 @@ const RedistRecord* ScheduleExecutor::push_record(const TermPlan& t) const {
   const TensorPlacement& src = t.placement_of(t.statement.output);
   const TensorPlacement& dst = rec->plan.destination;
   if (!uniform_blocks(src) || !uniform_blocks(dst)) return nullptr;
+  // every rank keeps its own block (whole self messages): the executor
+  // aliases the producer's buffer, nothing to push
+  bool all_self = src.dist.blocks == dst.dist.blocks && src.dist.extents == dst.dist.extents;
+  for (const Message& m : rec->plan.messages) all_self = all_self && m.self;
+  for (std::int64_t r = 0; all_self && r < pipe_.schedule.procs; ++r)
+    all_self = src.block_coords_of(r) == dst.block_coords_of(r);
+  if (all_self) return nullptr;
   std::int64_t reps = 1;
   for (std::size_t a = 0; a < dst.term_grid.dims.size(); ++a)
     if (std::find(dst.axes.begin(), dst.axes.end(), static_cast<int>(a)) == dst.axes.end())

@@ -45,6 +45,8 @@ Options read_env() {
   if (const char* v = std::getenv("EB_GEMM")) o.gemm = std::atoi(v);
   if (const char* v = std::getenv("EB_FUSE_REDIST")) o.fuse_redistribution = v[0] != '0';
   if (const char* v = std::getenv("EB_CHAIN_TERMS")) o.chain_terms = v[0] != '0';
+  if (const char* v = std::getenv("EB_CHAIN_FLAGS")) o.chain_flags = std::atoi(v);
+  if (const char* v = std::getenv("EB_CHAIN_LAG")) o.chain_lag = std::atoi(v);
   return o;
 }
 

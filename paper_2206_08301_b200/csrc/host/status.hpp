@@ -70,7 +70,12 @@ struct Options {
   int fuse_ttm2 = 1;      // executor: TTM pairs on eb_ttm2 (0: two eb_contract launches)
   int gemm = 0;           // wide GEMM steps: 0 auto, 1 GEMM mode forced, 2 split-K chunks
   int fuse_redistribution = 1;  // executor: push TTM outputs into the next term's blocks
-  int chain_terms = 1;    // executor: chained TTM-pair terms in one launch (eb_ttm2_chain)
+  // executor: chained TTM-pair terms in one launch (eb_ttm2_chain).  Off by
+  // default: measured 1.73 vs 1.60 ms on C5 although t1 never
+  // reaches HBM (DRAM writes 534 MB -> 20 MB)
+  int chain_terms = 0;
+  int chain_flags = 7;    // eb_ttm2_chain cache policy bits (ttm2.cu ChainParams::flags)
+  int chain_lag = 1;      // eb_ttm2_chain: term B of slab p runs in group p + lag
 };
 const Options& options();
 

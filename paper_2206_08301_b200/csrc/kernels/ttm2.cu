@@ -732,10 +732,15 @@ struct ChainTerm {
 struct ChainParams {
   int64_t P, groups, gsize, items;  // gsize = A.mtiles + B.mtiles
   int G;
+  int lag;  // group g holds the A tiles of slab g and the B tiles of slab g - lag
   ChainTerm t[2];
   unsigned* done;  // [P] completed A tiles per slab (zeroed before launch)
+  // cache policy: bit 0 evict-first X loads, bit 1 evict-last t1 stores,
+  // bit 2 discard t1 lines once read (option chain_flags; measured A/B)
+  int flags;
 };
 
+constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 
@@ -759,22 +764,26 @@ __device__ __forceinline__ void st_hint_f64(double* p, double a, uint64_t hint) 
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a), "l"(hint) : "memory");
 }
 
-// item -> (term, slab p, row tile); term -1 = empty slot (group 0's B part,
-// group P's A part)
+// item -> (term, slab p, row tile); term -1 = empty slot (the B parts of the
+// first `lag` groups, the A parts of the last ones)
 __device__ __forceinline__ int chain_item(const ChainParams& c, int64_t item, int64_t& p,
                                           int64_t& tile) {
   const int64_t gi = item / c.gsize, r = item - gi * c.gsize;
+  if ((c.flags & 8) && r >= c.t[0].mtiles) return -1;  // timing probe: term A only
   if (r < c.t[0].mtiles) {
     p = gi;
     tile = r;
     return gi < c.P ? 0 : -1;
   }
-  p = gi - 1;
+  p = gi - c.lag;
   tile = r - c.t[0].mtiles;
-  return gi >= 1 ? 1 : -1;
+  return (gi >= c.lag && p < c.P) ? 1 : -1;
 }
 
-__global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
+constexpr int kChainWarps = WsCfg<1>::Warps + 1;  // + the release warp
+constexpr int kRel = 4;                           // stored-tile hand-over ring
+
+__global__ void __launch_bounds__(kChainWarps * 32, 1)
     ttm2_chain_kernel(const __grid_constant__ CUtensorMap xmap,
                       const __grid_constant__ CUtensorMap tmap, const ChainParams prm) {
   using W = WsCfg<1, true>;  // JP = 1, 4-deep t0 ring
@@ -785,6 +794,8 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
   __shared__ __align__(8) uint64_t empty_x[kStages];
   __shared__ __align__(8) uint64_t full_t[kT0Slots];
   __shared__ __align__(8) uint64_t empty_t[kT0Slots];
+  __shared__ __align__(8) uint64_t rel_full[kRel];   // step-1 warps: A tile stored
+  __shared__ __align__(8) uint64_t rel_empty[kRel];  // release warp: published
 
   const uint32_t raw = smem_addr(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -803,9 +814,38 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
       mbar_init(smem_addr(&full_t[s]), kS0);
       mbar_init(smem_addr(&empty_t[s]), kS1);
     }
+    for (int s = 0; s < kRel; ++s) {
+      mbar_init(smem_addr(&rel_full[s]), kS1);
+      mbar_init(smem_addr(&rel_empty[s]), 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
+
+  if (warp == kS0 + kS1 + 1) {
+    // ------------------------------------------------------ release warp
+    // Publishes each stored A tile at gpu scope (fence + release add on
+    // done[p]) so the step-1 warps never stall on the memory fence: the
+    // tile's stores are ordered before the add through the CTA-scope
+    // mbarrier hand-over and the gpu-scope fence (cumulativity).
+    if (lane == 0) {
+      uint32_t na = 0;
+      for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
+        int64_t p, tile;
+        if (chain_item(prm, item, p, tile) != 0) continue;
+        const int s = na % kRel;
+        // a sleeping poll: this warp shares an SM sub-partition with
+        // DMMA-saturated warps, a spinning one would steal their issue slots
+        while (!mbar_try_wait(smem_addr(&rel_full[s]), (na / kRel) & 1)) __nanosleep(200);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(prm.done + p) : "memory");
+        mbar_arrive(smem_addr(&rel_empty[s]));
+        ++na;
+      }
+    }
+    return;
+  }
 
   if (warp == kS0 + kS1) {
     // ------------------------------------------------------------ producer
@@ -818,7 +858,7 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
         int64_t p, tile;
         const int tt = chain_item(prm, item, p, tile);
         if (tt < 0) continue;
-        const ChainTerm& T = prm.t[tt];
+        const ChainTerm T = tt == 0 ? prm.t[0] : prm.t[1];  // static param operands
         if (tt == 1 && p > ready) {
           // every A tile of slab p stored (acquire), then order the async
           // proxy (TMA) after it
@@ -841,12 +881,11 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
             mbar_wait(smem_addr(&empty_x[st]), ((it / kStages) - 1) & 1);
           const uint32_t fb = smem_addr(&full_x[st]);
           mbar_expect_tx(fb, kXBytes);
+          const uint64_t hint = (prm.flags & 1) ? kEvictFirst : kEvictNormal;
           if (tt == 0)
-            tma_load_4d_hint(base + st * kXBytes, &xmap, fb, r0, 0, (int)(kc * kK), (int)p,
-                             kEvictFirst);
+            tma_load_4d_hint(base + st * kXBytes, &xmap, fb, r0, 0, (int)(kc * kK), (int)p, hint);
           else
-            tma_load_4d_hint(base + st * kXBytes, &tmap, fb, r0, 0, (int)(kc * kK), (int)p,
-                             kEvictFirst);
+            tma_load_4d_hint(base + st * kXBytes, &tmap, fb, r0, 0, (int)(kc * kK), (int)p, hint);
         }
       }
     }
@@ -878,7 +917,7 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
       int64_t p, tile;
       const int tt = chain_item(prm, item, p, tile);
       if (tt < 0) continue;
-      const ChainTerm& T = prm.t[tt];
+      const ChainTerm T = tt == 0 ? prm.t[0] : prm.t[1];
       if (tt != cur) {  // this term's U1 into registers
 #pragma unroll
         for (int b16 = 0; b16 < W::B16; ++b16)
@@ -912,7 +951,7 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
               dmma884(t[1][nj][0], t[1][nj][1], a2.y, u1[b16][s][nj]);
             }
           }
-        if (tt == 1) {
+        if (tt == 1 && (prm.flags & 4)) {
           // t1 lines of this stage are consumed (they sit in shared memory):
           // drop them from L2 without a write-back.  Box lines (j, kk) of
           // t1[p][j][4 kc + kk][r0 .. r0 + 15]; lane covers j = lane, lane + 32.
@@ -966,12 +1005,12 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
-  uint32_t it = 0;
+  uint32_t it = 0, na = 0;
   for (int64_t item = blockIdx.x; item < prm.items; item += prm.G) {
     int64_t p, tile;
     const int tt = chain_item(prm, item, p, tile);
     if (tt < 0) continue;
-    const ChainTerm& T = prm.t[tt];
+    const ChainTerm T = tt == 0 ? prm.t[0] : prm.t[1];
     const int64_t r0 = tile * kRows;
     for (int64_t kc = 0; kc < T.KC; ++kc, ++it) {
       double ub[2];
@@ -1000,7 +1039,7 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
     }
     // out[p][r][b][c]: A -> t1 (evict-last: term B reads it from L2),
     // B -> the final output
-    const uint64_t hint = tt == 0 ? kEvictLast : kEvictFirst;
+    const uint64_t hint = tt == 0 ? ((prm.flags & 2) ? kEvictLast : kEvictNormal) : kEvictNormal;
 #pragma unroll
     for (int ri = 0; ri < RW; ++ri) {
       const int64_t r = r0 + RW * w1 + ri;
@@ -1025,13 +1064,15 @@ __global__ void __launch_bounds__(WsCfg<1>::Warps * 32, 1)
       }
     }
     if (tt == 0) {
-      // release this A tile of slab p once all four step-1 warps stored it
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      asm volatile("bar.sync 3, %0;" ::"n"(kS1 * 32) : "memory");
-      if (w1 == 0 && lane == 0) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(prm.done + p) : "memory");
+      // hand the stored tile to the release warp (mbarrier arrive: release
+      // at CTA scope); the ring slot must have been published first
+      __syncwarp();
+      if (lane == 0) {
+        const int s = na % kRel;
+        if (na >= (uint32_t)kRel) mbar_wait(smem_addr(&rel_empty[s]), ((na / kRel) - 1) & 1);
+        mbar_arrive(smem_addr(&rel_full[s]));
       }
+      ++na;
     }
   }
 }
@@ -1084,10 +1125,12 @@ void run_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* ws, size_t ws
   prm.t[0] = chain_term(a);
   prm.t[1] = chain_term(b);
   prm.gsize = prm.t[0].mtiles + prm.t[1].mtiles;
-  prm.groups = a->P + 1;
+  prm.lag = std::max(1, options().chain_lag);
+  prm.groups = a->P + prm.lag;
   prm.items = prm.groups * prm.gsize;
   prm.G = sm_count();
   prm.done = static_cast<unsigned*>(ws);
+  prm.flags = options().chain_flags;
   EB_CUDA(cudaMemsetAsync(ws, 0, (size_t)a->P * sizeof(unsigned), st));
   const CUtensorMap xmap = ttm2_xmap(a->X, a);
   const CUtensorMap tmap = ttm2_xmap(b->X, b);
@@ -1096,7 +1139,7 @@ void run_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* ws, size_t ws
   main_kernel_begin(st);
   // a plain launch (no PDL): every CTA must be able to become resident for
   // the in-kernel slab dependencies
-  ttm2_chain_kernel<<<prm.G, W::Warps * 32, W::Smem, st>>>(xmap, tmap, prm);
+  ttm2_chain_kernel<<<prm.G, kChainWarps * 32, W::Smem, st>>>(xmap, tmap, prm);
   EB_CUDA(cudaGetLastError());
   main_kernel_end(st);
   count_launch();

@@ -169,12 +169,13 @@ def test_ttmc_o5_fused_terms(eb, P, opts):
     assert [t["output"] for t in plan["schedule"]["terms"]] == ["t1", "out"]
     ops = oracle.seeded_inputs(e, ext, 5)
     want = _ttmc_o5_chain(ext, ops)
+    opts("chain_terms", 1)
     ex = eb.Executor(e, ext, P)
     ex.stage(ops)
     ex.run()
     st = ex.stats()
-    # the two terms chain into one eb_ttm2_chain launch per rank where the t1
-    # hand-over is a whole-block self message (P = 1, 2, 8 here), else two
+    # with chaining on, the two terms run as one eb_ttm2_chain launch per rank
+    # where the t1 hand-over is a whole-block self message, else two
     plan_r = json.loads(eb.plan_json(e, ext, P, include_messages=True))
     selfonly = all(m["self"] for r in plan_r["schedule"]["redistributions"]
                    for m in r["plan"]["messages"])
@@ -963,6 +964,7 @@ def test_ttm2_chain_both_terms_one_launch(eb, P, ext, opts):
     e = "ijklm,jb,kc,ld,me->ibcde"
     ops = oracle.seeded_inputs(e, ext, 71)
     want = _ttmc_o5_chain(ext, ops)
+    opts("chain_terms", 1)
     ex = eb.Executor(e, ext, P)
     ex.stage(ops)
     for _ in range(3):
