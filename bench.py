@@ -441,12 +441,19 @@ def main():
                          "dimtree: modes 0 and 1 from one pass over X (T = X x_k C folded "
                          "into both outputs, eb_exec_run_pair), mode 2 as before — 2/3 of "
                          "the DMMA flops for the same three outputs")
-    ap.add_argument("--transport", default="auto", choices=["auto", "virtual", "nccl"],
+    ap.add_argument("--transport", default="auto", choices=["auto", "virtual", "nccl", "peer"],
                     help="auto: NCCL (one process per GPU) when WORLD_SIZE > 1, else the "
-                         "in-device virtual-rank transport; nccl forces the NCCL path")
+                         "in-device virtual-rank transport; nccl forces the NCCL path; peer: "
+                         "one process per rank over CUDA-IPC peer memory")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="functional check of the N-rank path on fewer GPUs: ranks share the "
+                         "visible devices (rank r on device r mod count), peer transport, gloo "
+                         "for the timing plumbing — the numbers are NOT a multi-GPU measurement")
     args = ap.parse_args()
+    if args.share_gpu:
+        args.transport = "peer"
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
-        return _self_launch(args.gpus)
+        return _self_launch(args.gpus, args.share_gpu)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -461,9 +468,14 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    ndev = max(torch.cuda.device_count(), 1)
+    dev = local % ndev if args.share_gpu else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:  # NCCL refuses two ranks on one GPU; gloo carries the plumbing
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     P = world
     import paper_2206_08301_b200 as eb
     from paper_2206_08301_b200 import _capi
@@ -476,24 +488,33 @@ def main():
     if dimtree:
         label += "; dimension tree: modes 0+1 in one pass over X (eb_exec_run_pair), mode 2 " \
                  "separately — same outputs, 2/3 of the DMMA flops"
-    use_nccl = world > 1 or args.transport == "nccl"
-    nccl_id = None
-    if world > 1:
+    peer = args.transport == "peer"
+    use_nccl = (world > 1 or args.transport == "nccl") and not peer
+    nccl_id, group = None, None
+    if world > 1 and use_nccl:
         obj = [eb.Executor.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     elif use_nccl:
         nccl_id = eb.Executor.nccl_unique_id()
+    if peer:
+        import uuid
+        obj = [f"/eb_bench_{uuid.uuid4().hex[:16]}" if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        group = obj[0]
+    ranked = use_nccl or peer
     stream = torch.cuda.Stream()
     execs, inputs, grids, flops_tree = [], [], [], 0
     x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
     # one process per GPU: stage only this rank's boxes (EB_BENCH_BLOCKS=1
     # forces it for a single NCCL rank, to exercise the path on one GPU)
-    blockmode = world > 1 or (use_nccl and os.environ.get("EB_BENCH_BLOCKS") == "1")
+    blockmode = world > 1 or (ranked and os.environ.get("EB_BENCH_BLOCKS") == "1")
     for mi, (e, ext, build) in enumerate(modes):
         if mi == 0:
-            ex = eb.Executor(e, ext, P, 1024.0, rank if use_nccl else -1, nccl_id,
-                             stream=stream.cuda_stream)
+            ex = eb.Executor(e, ext, P, 1024.0, rank if ranked else -1, nccl_id,
+                             stream=stream.cuda_stream, transport="peer" if peer else "nccl",
+                             group=group)
         else:  # same ranks / same NCCL communicator as mode 0
             ex = eb.Executor(e, ext, stream=stream.cuda_stream, like=execs[0])
         shared = False
@@ -561,9 +582,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(ms)
     ms_step = ms / args.steps
     value = flops_tree / (ms_step * 1e-3) / 1e9
 
@@ -586,7 +605,7 @@ def main():
             # bytes this rank copies: its blocks of every operand it stages
             h2d += (sum(a.nbytes for a in _stage_list(ins, sh, dimtree and ex_ is execs[1])
                         if a is not None) if blockmode else
-                    _staged_bytes(ex_, ins, P, rank if use_nccl else -1, eb, skip0=sh,
+                    _staged_bytes(ex_, ins, P, rank if ranked else -1, eb, skip0=sh,
                                   skip2=dimtree and ex_ is execs[1]))
         d2h = sum(o.nbytes for o in outs) if rank == 0 else 0
         reps = max(1, min(args.steps, 3))
@@ -603,9 +622,7 @@ def main():
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / reps
         if world > 1:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = _max_over_ranks(dt)
         e2e = {"value": flops_tree / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
                "host_buffers": "pinned" if (world == 1 or blockmode) else "pageable"}
@@ -689,7 +706,9 @@ def main():
         "data": "synthetic: reference random_tensor streams (mt19937_64, seed 0 for X, "
                 "factor seeds 1/2/3), generated on the host",
         "config": {"workload": label, "procs": P, "fast_mem": 1024, "grids": grids,
-                   "transport": "nccl" if use_nccl else "virtual",
+                   "transport": "nccl" if use_nccl else ("peer" if peer else "virtual"),
+                   **({"shared_gpu": "ranks share the visible GPUs: a functional check, "
+                                     "not a multi-GPU timing"} if args.share_gpu else {}),
                    "tree_flops_per_step": flops_tree,
                    "l2": "inputs larger than L2 (X is %.2f GB per GPU vs 126 MB L2), no flush "
                          "needed" % (_x_bytes(modes[:1], P) / 1e9)},
@@ -709,14 +728,26 @@ def main():
     return 0
 
 
-def _self_launch(n):
+def _max_over_ranks(x: float) -> float:
+    """Max over ranks (the timing rule), on whichever backend carries the
+    plumbing (NCCL: a device tensor; gloo: a host one)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _self_launch(n, share_gpu=False):
     """`bench.py --gpus N` without torchrun: re-launch as N ranks (one process
     per GPU) with torch.distributed.run; fail loudly when the box has fewer
-    than N GPUs instead of running one rank."""
+    than N GPUs instead of running one rank (unless --share-gpu asks for the
+    functional check on fewer GPUs)."""
     import socket
     import torch
     have = torch.cuda.device_count()
-    if have < n:
+    if have < n and not share_gpu:
         print(f"bench.py: --gpus {n} needs {n} GPUs, this box has {have}", file=sys.stderr)
         return 2
     s = socket.socket()
@@ -769,9 +800,7 @@ def _time_dimtree(eb, execs, inputs, stream, args, world, flops_tree):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(ms)
     ms_step = ms / args.steps
     return {"value": flops_tree / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s",
             "ms_per_step": ms_step,
