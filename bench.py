@@ -556,8 +556,8 @@ def main():
     if world > 1:
         dist.barrier()
 
-    clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
-                          int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    clocks = ClockSampler(dev if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                          int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[dev]))
     clocks.start()
     L.eb_timer_enable(1)
     L.eb_timer_collect(None, None)
