@@ -73,3 +73,49 @@ def test_random_block_is_the_box_of_random_tensor(eb):
         got = eb.random_block(11, g, base, shape)
         want = full[tuple(slice(a, a + n) for a, n in zip(base, shape))]
         assert np.array_equal(got, want)
+
+
+def test_path_options_set_and_validated_without_gpu(eb):
+    """eb_set_option: the path options are plain host state (read once from
+    EB_* at load); unknown names and out-of-range values are rejected."""
+    from paper_2206_08301_b200 import EinplanError
+    for name, good in (("no_fused_tma", 1), ("no_rf", 1), ("rf_cfg", "64x1"),
+                       ("ttm2_variant", 2), ("fuse_ttm2", 0), ("gemm", 1),
+                       ("fuse_redistribution", 0), ("chain_terms", 1)):
+        eb.set_option(name, good)
+    for name, value in (("no_fused_tma", 0), ("no_rf", 0), ("rf_cfg", "auto"),
+                        ("ttm2_variant", 0), ("fuse_ttm2", 1), ("gemm", 0),
+                        ("fuse_redistribution", 1), ("chain_terms", 0)):
+        eb.set_option(name, value)
+    for name, bad in (("no_such_option", 1), ("ttm2_variant", 7), ("gemm", 3),
+                      ("rf_cfg", "sixteen")):
+        with pytest.raises(EinplanError):
+            eb.set_option(name, bad)
+
+
+def test_random_stream_continues_the_reference_stream(eb):
+    """RandomStream (eb_rng_*): consecutive fills are consecutive slices of
+    random_tensor's mt19937_64 stream (tensor.cpp:55-63), also from a skip."""
+    import numpy as np
+    import oracle
+    want = oracle.random_tensor((3000,), 5)
+    rs = eb.RandomStream(5)
+    a = rs.fill(np.empty(1234))
+    b = rs.fill(np.empty(1766))
+    assert np.array_equal(np.concatenate([a, b]), want)
+    c = eb.RandomStream(5, skip=1000).fill(np.empty(500))
+    assert np.array_equal(c, want[1000:1500])
+
+
+def test_python_mirror_rejects_bad_shapes_before_the_abi(eb):
+    """Executor.stage / gather check operand counts, shapes and output buffers
+    in Python (no host pointer with the wrong size crosses the C ABI)."""
+    import numpy as np
+    ex = eb.Executor.__new__(eb.Executor)  # no device: exercise the checks only
+    ex._shapes = [(4, 5, 6), (5, 3), (6, 3)]
+    ex._h = None
+    ex.rank = -1
+    with pytest.raises(ValueError):
+        ex.stage([np.zeros((4, 5, 6))])  # operand count
+    with pytest.raises(ValueError):
+        ex.stage([np.zeros((4, 5, 7)), np.zeros((5, 3)), np.zeros((6, 3))])  # shape
