@@ -436,6 +436,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the secondary C1/C3/C4/C5 lines embedded in the default C2 run")
     ap.add_argument("--sweep", default="modes", choices=["modes", "dimtree"],
                     help="C2 only. modes: the reference's three einsums, one schedule each; "
                          "dimtree: modes 0 and 1 from one pass over X (T = X x_k C folded "
@@ -721,11 +723,37 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args.config)
+    if world == 1 and args.config == "C2" and not args.no_other_configs:
+        line["other_configs"] = _other_configs(args)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _other_configs(args):
+    """The other BASELINE configs measured in the same run (after the timed
+    headline, one subprocess each: `bench.py --config C --no-e2e
+    --no-cpu-baseline`), summarised: value, ms/step, the binding roof and
+    the fraction of it, the clocks they ran at."""
+    out = {}
+    for c in ("C1", "C3", "C4", "C5"):
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", c, "--steps",
+               str(max(args.steps, 10)), "--warmup", str(max(args.warmup, 3)), "--no-e2e",
+               "--no-cpu-baseline"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            l = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+            ro = l["roofline"]
+            out[c] = {"workload": l["config"]["workload"], "value": l["value"], "unit": l["unit"],
+                      "ms_per_step": l["ms_per_step"], "bound": ro["bound"],
+                      "achieved": ro["achieved"], "peak": ro["peak"], "roof_unit": ro["unit"],
+                      "frac": ro["frac"], "kernel": ro.get("kernel"),
+                      "gpu_launches": l.get("gpu_launches"), "clocks": l.get("clocks")}
+        except Exception as e:  # reported, never fatal for the headline
+            out[c] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    return out
 
 
 def _max_over_ranks(x: float) -> float:
