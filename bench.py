@@ -443,10 +443,13 @@ def main():
                          "dimtree: modes 0 and 1 from one pass over X (T = X x_k C folded "
                          "into both outputs, eb_exec_run_pair), mode 2 as before — 2/3 of "
                          "the DMMA flops for the same three outputs")
-    ap.add_argument("--transport", default="auto", choices=["auto", "virtual", "nccl", "peer"],
-                    help="auto: NCCL (one process per GPU) when WORLD_SIZE > 1, else the "
-                         "in-device virtual-rank transport; nccl forces the NCCL path; peer: "
-                         "one process per rank over CUDA-IPC peer memory")
+    ap.add_argument("--transport", default="auto",
+                    choices=["auto", "virtual", "nccl", "peer", "hybrid"],
+                    help="auto: hybrid when WORLD_SIZE > 1 (one process per GPU: MTTKRP "
+                         "allreduces on NCCL split communicators, TTMc redistributions fused "
+                         "into the producing kernel over CUDA-IPC peer memory), else the "
+                         "in-device virtual-rank transport; nccl: NCCL only (grouped "
+                         "send/recv redistributions); peer: peer memory only")
     ap.add_argument("--share-gpu", action="store_true",
                     help="functional check of the N-rank path on fewer GPUs: ranks share the "
                          "visible devices (rank r on device r mod count), peer transport, gloo "
@@ -490,8 +493,11 @@ def main():
     if dimtree:
         label += "; dimension tree: modes 0+1 in one pass over X (eb_exec_run_pair), mode 2 " \
                  "separately — same outputs, 2/3 of the DMMA flops"
-    peer = args.transport == "peer"
-    use_nccl = (world > 1 or args.transport == "nccl") and not peer
+    if args.transport == "auto" and world > 1:
+        args.transport = "hybrid"
+    peer = args.transport in ("peer", "hybrid")
+    use_nccl = (world > 1 or args.transport == "nccl" or args.transport == "hybrid") and \
+        args.transport != "peer"
     nccl_id, group = None, None
     if world > 1 and use_nccl:
         obj = [eb.Executor.nccl_unique_id() if rank == 0 else None]
@@ -515,8 +521,9 @@ def main():
     for mi, (e, ext, build) in enumerate(modes):
         if mi == 0:
             ex = eb.Executor(e, ext, P, 1024.0, rank if ranked else -1, nccl_id,
-                             stream=stream.cuda_stream, transport="peer" if peer else "nccl",
-                             group=group)
+                             stream=stream.cuda_stream,
+                             transport=args.transport if args.transport in ("peer", "hybrid")
+                             else "nccl", group=group)
         else:  # same ranks / same NCCL communicator as mode 0
             ex = eb.Executor(e, ext, stream=stream.cuda_stream, like=execs[0])
         shared = False
@@ -708,7 +715,8 @@ def main():
         "data": "synthetic: reference random_tensor streams (mt19937_64, seed 0 for X, "
                 "factor seeds 1/2/3), generated on the host",
         "config": {"workload": label, "procs": P, "fast_mem": 1024, "grids": grids,
-                   "transport": "nccl" if use_nccl else ("peer" if peer else "virtual"),
+                   "transport": (args.transport if args.transport in ("peer", "hybrid") else
+                                 "nccl" if use_nccl else "virtual"),
                    **({"shared_gpu": "ranks share the visible GPUs: a functional check, "
                                      "not a multi-GPU timing"} if args.share_gpu else {}),
                    "tree_flops_per_step": flops_tree,

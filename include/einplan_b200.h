@@ -262,6 +262,13 @@ int eb_exec_create(const char* einsum, const char* dims, int64_t procs, double f
  * peers on the host.  Every rank must call eb_exec_run / eb_exec_gather. */
 int eb_exec_create_peer(const char* einsum, const char* dims, int64_t procs, double fast_mem,
                         int64_t rank, const char* group, void* stream, eb_exec** out);
+/* hybrid (one process per GPU): the peer transport's mapped heaps and fused
+ * redistributions, with the MTTKRP allreduces on NCCL (ncclCommSplit groups,
+ * asynchronous on the communication stream); both a group name and a
+ * 128-byte ncclUniqueId */
+int eb_exec_create_hybrid(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                          int64_t rank, const char* group, const void* nccl_id, void* stream,
+                          eb_exec** out);
 /* a second executor over the same ranks and the same communicator as `peer`
  * (an ncclUniqueId initialises exactly one communicator): e.g. the three
  * MTTKRP modes of a sweep on one process group */

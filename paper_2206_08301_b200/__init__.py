@@ -209,7 +209,9 @@ class Executor:
     takes ``nccl_id`` (128 bytes) from :meth:`nccl_unique_id` on rank 0;
     ``transport="peer"`` meets the other ranks' processes in the POSIX
     shared-memory segment ``group`` (e.g. "/eb_job42") and exchanges over
-    CUDA IPC peer memory — several processes may share one GPU.
+    CUDA IPC peer memory — several processes may share one GPU;
+    ``transport="hybrid"`` (one GPU per process) is the peer transport with
+    its allreduces on NCCL (needs both ``group`` and ``nccl_id``).
     """
 
     def __init__(self, einsum: str, dims, procs: int = 1, fast_mem: float = 1024.0,
@@ -232,8 +234,16 @@ class Executor:
             _capi.check(L.eb_exec_create_peer(einsum.encode(), dims_string(dims).encode(), procs,
                                               fast_mem, rank, group.encode(),
                                               ctypes.c_void_p(stream or 0), ctypes.byref(self._h)))
+        elif rank >= 0 and transport == "hybrid":
+            if not group or nccl_id is None:
+                raise ValueError("Executor(transport='hybrid') needs a group name and an nccl_id")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            _capi.check(L.eb_exec_create_hybrid(einsum.encode(), dims_string(dims).encode(),
+                                                procs, fast_mem, rank, group.encode(), idbuf,
+                                                ctypes.c_void_p(stream or 0),
+                                                ctypes.byref(self._h)))
         else:
-            if transport not in ("nccl", "peer"):
+            if transport not in ("nccl", "peer", "hybrid"):
                 raise ValueError(f"unknown transport {transport!r}")
             idbuf = (ctypes.create_string_buffer(bytes(nccl_id), 128)
                      if nccl_id is not None else None)

@@ -61,7 +61,7 @@ EXPORTS = [
     "eb_group_sum", "eb_group_sum_into", "eb_copy_box", "eb_set_option", "eb_exec_create_peer",
     "eb_exec_stage_region", "eb_rng_create", "eb_rng_fill", "eb_rng_destroy", "eb_mem_in_use", "eb_pad_rows", "eb_permute",
     "eb_contract_scatter", "eb_ttm2_scatter", "eb_exec_fused_redistributions",
-    "eb_ttm2_chain", "eb_ttm2_chain_workspace", "eb_einsum_generic", "eb_random_fill_host",
+    "eb_ttm2_chain", "eb_ttm2_chain_workspace", "eb_exec_create_hybrid", "eb_einsum_generic", "eb_random_fill_host",
     "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
@@ -143,6 +143,8 @@ def lib():
         _sig(L, "eb_exec_create_peer", ctypes.c_int,
              [c, c, _i64, ctypes.c_double, _i64, c, _vp, ctypes.POINTER(_vp)])
         _sig(L, "eb_set_option", ctypes.c_int, [c, c])
+        _sig(L, "eb_exec_create_hybrid", ctypes.c_int,
+             [c, c, _i64, ctypes.c_double, _i64, c, _vp, _vp, ctypes.POINTER(_vp)])
         _sig(L, "eb_group_sum", ctypes.c_int, [ctypes.POINTER(_dp), ctypes.c_int, _i64, _vp])
         _sig(L, "eb_group_sum_into", ctypes.c_int,
              [ctypes.POINTER(_dp), ctypes.c_int, _i64, _dp, _vp])

@@ -457,6 +457,34 @@ int eb_exec_create_peer(const char* einsum, const char* dims, int64_t procs, dou
   });
 }
 
+int eb_exec_create_hybrid(const char* einsum, const char* dims, int64_t procs, double fast_mem,
+                          int64_t rank, const char* group, const void* nccl_id, void* stream,
+                          eb_exec** out) {
+  return exec_guard([&] {
+    if (!out || !group || !nccl_id) throw eb::InvalidError("eb_exec_create_hybrid: null argument");
+    *out = nullptr;
+    if (rank < 0 || rank >= procs)
+      throw eb::InvalidError("eb_exec_create_hybrid: rank outside 0..procs-1");
+#ifdef EB_HAVE_NCCL
+    auto h = std::make_unique<eb_exec>();
+    h->fast_mem = fast_mem;
+    h->stream = static_cast<cudaStream_t>(stream);
+    Pipeline pipe = make_pipeline(make_spec(einsum, dims), procs, fast_mem);
+    auto shared = gpu::PeerShared::attach_shm(group, static_cast<int>(procs));
+    auto comm = std::make_shared<gpu::PeerComm>(shared, static_cast<int>(rank));
+    h->transport = std::make_shared<gpu::PeerTransport>(
+        comm, procs, std::make_unique<gpu::NcclTransport>(nccl_id, procs, rank));
+    h->procs = procs;
+    h->exec = std::make_unique<gpu::ScheduleExecutor>(std::move(pipe), h->transport.get(),
+                                                      h->stream);
+    *out = h.release();
+#else
+    (void)einsum; (void)dims; (void)fast_mem; (void)stream;
+    throw eb::DeviceError("built without NCCL");
+#endif
+  });
+}
+
 int eb_exec_create_like(const char* einsum, const char* dims, double fast_mem, eb_exec* peer,
                         void* stream, eb_exec** out) {
   return exec_guard([&] {

@@ -205,8 +205,9 @@ void VirtualTransport::redistribute(const RedistributionPlan& plan,
 
 // ---- peer memory ----
 
-PeerTransport::PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks)
-    : comm_(std::move(comm)), nranks_(nranks) {
+PeerTransport::PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks,
+                             std::unique_ptr<Transport> allreduce_via)
+    : comm_(std::move(comm)), nranks_(nranks), allreduce_via_(std::move(allreduce_via)) {
   if (comm_->nranks() != nranks)
     fail(errc::invalid_argument, "peer transport: group of " + std::to_string(comm_->nranks()) +
                                      " ranks for a schedule of " + std::to_string(nranks));
@@ -216,6 +217,8 @@ std::int64_t PeerTransport::allreduce(const TensorPlacement& place, const Reduct
                                       std::vector<DevBlock>& blocks,
                                       std::vector<std::int64_t>& per_rank_sent, cudaStream_t st) {
   if (grp.depth <= 1) return 0;
+  if (allreduce_via_)  // hybrid: NCCL on the split communicator, in place, asynchronous
+    return allreduce_via_->allreduce(place, grp, blocks, per_rank_sent, st);
   std::int64_t volume = 0;
   const auto groups = reduction_groups(place, per_rank_sent, volume);
   const std::int64_t me = comm_->rank();
@@ -1734,21 +1737,21 @@ ExecChoice choose_execution(std::int64_t procs) {
   const std::set<int> distinct(c.dev.begin(), c.dev.end());
   c.transport = "peer";
 #ifdef EB_HAVE_NCCL
-  if (procs > 1 && distinct.size() == c.dev.size()) c.transport = "nccl";
+  if (procs > 1 && distinct.size() == c.dev.size()) c.transport = "hybrid";
 #endif
   if (const char* t = std::getenv("EINPLAN_TRANSPORT")) {
     const std::string ts(t);
     if (ts == "peer") {
       c.transport = "peer";
-    } else if (ts == "nccl") {
+    } else if (ts == "nccl" || ts == "hybrid") {
 #ifndef EB_HAVE_NCCL
       fail(errc::invalid_argument, "EINPLAN_TRANSPORT=nccl: built without NCCL");
 #endif
       if (distinct.size() != c.dev.size())
-        fail(errc::invalid_argument, "EINPLAN_TRANSPORT=nccl needs one distinct GPU per rank");
-      c.transport = "nccl";
+        fail(errc::invalid_argument, "EINPLAN_TRANSPORT=" + ts + " needs one distinct GPU per rank");
+      c.transport = ts;
     } else {
-      fail(errc::invalid_argument, "EINPLAN_TRANSPORT: \"nccl\" or \"peer\"");
+      fail(errc::invalid_argument, "EINPLAN_TRANSPORT: \"nccl\", \"hybrid\" or \"peer\"");
     }
   }
   return c;
@@ -1771,9 +1774,8 @@ void run_threads(const Pipeline& pipe, const std::vector<const double*>& globals
   const int procs = static_cast<int>(pipe.schedule.procs);
   std::shared_ptr<gpu::PeerShared> shared;
   std::vector<void*> comms(static_cast<std::size_t>(procs), nullptr);
-  if (ch.transport == "peer") {
-    shared = gpu::PeerShared::for_threads(procs);
-  } else {
+  if (ch.transport == "peer" || ch.transport == "hybrid") shared = gpu::PeerShared::for_threads(procs);
+  if (ch.transport != "peer") {
 #ifdef EB_HAVE_NCCL
     std::vector<ncclComm_t> c(static_cast<std::size_t>(procs));
     const ncclResult_t r = ncclCommInitAll(c.data(), procs, ch.dev.data());
@@ -1788,14 +1790,18 @@ void run_threads(const Pipeline& pipe, const std::vector<const double*>& globals
     std::unique_ptr<gpu::Transport> tp;
     try {
       cuda_ok(cudaSetDevice(ch.dev[static_cast<std::size_t>(r)]), "cudaSetDevice");
-      if (shared) {
-        tp = std::make_unique<gpu::PeerTransport>(std::make_shared<gpu::PeerComm>(shared, r), procs);
-      } else {
+      std::unique_ptr<gpu::Transport> nccl;
 #ifdef EB_HAVE_NCCL
-        tp = std::make_unique<gpu::NcclTransport>(comms[static_cast<std::size_t>(r)], procs, r);
+      if (comms[static_cast<std::size_t>(r)]) {
+        nccl = std::make_unique<gpu::NcclTransport>(comms[static_cast<std::size_t>(r)], procs, r);
         comms[static_cast<std::size_t>(r)] = nullptr;  // owned by the transport now
-#endif
       }
+#endif
+      if (shared)  // peer, or hybrid: NCCL allreduce + fused redistribution over peer memory
+        tp = std::make_unique<gpu::PeerTransport>(std::make_shared<gpu::PeerComm>(shared, r),
+                                                  procs, std::move(nccl));
+      else
+        tp = std::move(nccl);
       cudaStream_t st = nullptr;
       cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
       {

@@ -100,9 +100,15 @@ class VirtualTransport final : public Transport {
 //     source's heap with strided box copies (redistribute.cpp:185-206) —
 //     no pack, no unpack, one pass over the link;
 //   gather: rank 0 reads the canonical blocks from the peers' heaps.
+//
+// Hybrid (the default for one process per GPU): a PeerTransport whose
+// allreduces go to an NCCL communicator (ncclCommSplit groups, asynchronous
+// on the communication stream) while the redistributions stay fused into the
+// producing kernels over the mapped heaps.
 class PeerTransport final : public Transport {
  public:
-  PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks);
+  PeerTransport(std::shared_ptr<PeerComm> comm, std::int64_t nranks,
+                std::unique_ptr<Transport> allreduce_via = nullptr);
   bool owns(std::int64_t r) const override { return r == comm_->rank(); }
   bool is_virtual() const override { return false; }
   bool peer_mapped() const override { return true; }
@@ -115,10 +121,12 @@ class PeerTransport final : public Transport {
                       cudaStream_t st) override;
   void gather_done(std::vector<DevBlock>& blocks, cudaStream_t st) override;
   PeerComm& comm() { return *comm_; }
+  bool hybrid() const { return allreduce_via_ != nullptr; }
 
  private:
   std::shared_ptr<PeerComm> comm_;
   std::int64_t nranks_;
+  std::unique_ptr<Transport> allreduce_via_;
 };
 
 #ifdef EB_HAVE_NCCL

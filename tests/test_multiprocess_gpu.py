@@ -136,3 +136,26 @@ def test_virtual_runs_keep_the_pool_flat(eb):
         ex.gather()
         mem.append(eb.mem_in_use())
     assert mem[-1] <= mem[1], mem
+
+
+def test_hybrid_transport_single_rank(eb, monkeypatch):
+    """The hybrid transport (the default for one process per GPU: NCCL
+    allreduce + fused redistribution over peer memory) as rank 0 of 1 — the
+    only NCCL world this one-GPU pool can host — through the executor and
+    through einplan_run_json."""
+    import uuid
+    for e, ext in (("ijk,ja,ka->ia", dict(i=64, j=64, k=64, a=16)),
+                   ("ijk,jb,kc->ibc", dict(i=96, j=96, k=96, b=24, c=24))):
+        ops = oracle.seeded_inputs(e, ext, 13)
+        ex = eb.Executor(e, ext, 1, rank=0, transport="hybrid",
+                         group=f"/eb_h{uuid.uuid4().hex[:12]}",
+                         nccl_id=eb.Executor.nccl_unique_id())
+        ex.stage(ops)
+        for _ in range(2):
+            ex.run()
+            got = ex.gather()
+            assert oracle.normwise_error(got, oracle.naive_evaluate(e, ext, ops).ravel()) <= TOL
+    monkeypatch.setenv("EINPLAN_TRANSPORT", "hybrid")
+    st, rep = eb.Session("ijk,jb,kc->ibc", dict(i=24, j=40, k=36, b=8, c=6)).run_json(1, seed=2)
+    assert st == 0
+    assert json.loads(rep)["execution"]["transport"] == "hybrid"
