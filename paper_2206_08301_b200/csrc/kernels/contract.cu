@@ -76,6 +76,7 @@ struct ContractParams {
   // one TMA box per operand per stage: the 16-wide column blocks are a tensor
   // dimension of the maps (contiguous extent a multiple of 16)
   int fused_tma;
+  int64_t outer;   // BATCHED COL: real outer count (O * OS may exceed it)
   // BATCHED COL: scatter epilogue (sc.nd > 0) — stores go to the next term's
   // destination blocks instead of `out`
   eb_scatter sc;
@@ -343,7 +344,8 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
     contract_kernel(const __grid_constant__ CUtensorMap xmap,
                     const __grid_constant__ CUtensorMap umap, const ContractParams prm) {
   static_assert(KD % (16 * KS) == 0, "each k-split group owns whole 16-deep groups");
-  static_assert(!BATCHED || OS == 1, "BATCHED stages one outer index");
+  static_assert(!BATCHED || OS == 1 || COL,
+                "BATCHED stages one outer index (COL: OS outer indices of a narrow M)");
   constexpr int MT = NWM * WM;
   constexpr int MI = WM / 8;  // m8 tiles per warp
   constexpr int NCW = NWM * KS * OS;
@@ -784,8 +786,19 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[st]));
     }
+    // BATCHED COL with OS > 1: this warp's unit is outer index o * OS + os
+    const int64_t ou = (BATCHED && COL) ? o * OS + os : o;
+    if constexpr (BATCHED && COL && OS > 1) {
+      if (ou >= prm.outer) {  // the last group's missing outer indices (zero-filled loads)
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        continue;
+      }
+    }
     if constexpr (SC) {  // fused redistribution: push to the destination blocks
-      scatter_unit<MI, NT, MT, WM, VC>(acc, prm, sc_tab, mt, o, wm, g, l);
+      scatter_unit<MI, NT, MT, WM, VC>(acc, prm, sc_tab, mt, ou, wm, g, l);
       continue;
     }
     if constexpr (BATCHED && VC) {
@@ -794,7 +807,7 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
       for (int i = 0; i < MI; ++i) {
         const int64_t row = mt * MT + wm * WM + vc_row(i, g);
         if (row < prm.M) {
-          double* dst = prm.out + (o * prm.M + row) * prm.ldo + prm.col0;
+          double* dst = prm.out + (ou * prm.M + row) * prm.ldo + prm.col0;
 #pragma unroll
           for (int q = 0; q < NT / 2; ++q)
 #pragma unroll
@@ -821,7 +834,7 @@ __global__ void __launch_bounds__(WS ? 384 : (NWM * KS * OS + 1) * 32, 1)
       for (int i = 0; i < MI; ++i) {
         const int64_t row = mt * MT + wm * WM + i * 8 + g;
         if (row < prm.M) {
-          double* dst = COL ? prm.out + (o * prm.M + row) * prm.ldo + prm.col0
+          double* dst = COL ? prm.out + (ou * prm.M + row) * prm.ldo + prm.col0
                             : prm.out + row * prm.ldo + cbase;
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
@@ -1077,8 +1090,15 @@ Plan plan_of(const eb_contract_desc* d) {
   if (p.batched) {
     // wide N (compute-bound TTM): 8 warps x 16 rows, two warps per SMSP
     // (C4 step 0: 92 % vs 80 % of peak); narrow N (HBM-bound): 4 x 32.
+    // Narrow M (<= 32 rows: e.g. C4's second TTM at P = 8, whose b block is
+    // 16) stages OS outer indices per tile so no warp computes padding rows:
+    // 1 x 16 rows x 8 outer indices, or 2 x 16 x 4.
     if (rows >= 128 && p.nt >= 4) {
       p.nwm = 8; p.wm = 16;
+    } else if (rows <= 16 && d->P >= 8) {
+      p.nwm = 1; p.wm = 16; p.os = 8;
+    } else if (rows <= 32 && d->P >= 4) {
+      p.nwm = 2; p.wm = 16; p.os = 4;
     } else {
       p.nwm = 4; p.wm = rows >= 128 ? 32 : 16;
     }
@@ -1092,7 +1112,8 @@ Plan plan_of(const eb_contract_desc* d) {
   }
   p.mt = p.nwm * p.wm;
   p.kin = p.col ? d->Q : d->L;
-  p.O = (p.col ? d->P : d->P * d->Q) / p.os;  // outer-index groups
+  p.O = p.batched ? cdiv(d->P, p.os)                      // BATCHED: ragged last group
+                  : (p.col ? d->P : d->P * d->Q) / p.os;  // outer-index groups
   p.KC = cdiv(p.kin, p.kd);
   p.mtiles = cdiv(rows, p.mt);
   const int sms = sm_count();
@@ -1178,11 +1199,15 @@ void launch_variant(const Plan& p, int nt, const CUtensorMap& xm, const CUtensor
                     const ContractParams& prm, cudaStream_t st) {
   if (p.gemm) return launch_t<false, true, 8, 16, 1, 32, 1, 8>(xm, um, prm, st);
   if (p.batched && prm.sc.nd > 0) {  // the scatter-epilogue instantiations
+    if (p.os == 8) return dispatch_nt<true, true, 1, 16, 1, 32, 8, 1, 8, true>(nt, xm, um, prm, st);
+    if (p.os == 4) return dispatch_nt<true, true, 2, 16, 1, 32, 4, 1, 8, true>(nt, xm, um, prm, st);
     if (p.nwm == 8) return dispatch_nt<true, true, 8, 16, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
     if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
     return dispatch_nt<true, true, 4, 16, 1, 32, 1, 1, 8, true>(nt, xm, um, prm, st);
   }
   if (p.batched) {
+    if (p.os == 8) return dispatch_nt<true, true, 1, 16, 1, 32, 8, 1, 8>(nt, xm, um, prm, st);
+    if (p.os == 4) return dispatch_nt<true, true, 2, 16, 1, 32, 4, 1, 8>(nt, xm, um, prm, st);
     if (p.nwm == 8) return dispatch_nt<true, true, 8, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
     if (p.wm == 32) return dispatch_nt<true, true, 4, 32, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
     return dispatch_nt<true, true, 4, 16, 1, 32, 1, 1, 8>(nt, xm, um, prm, st);
@@ -1215,6 +1240,7 @@ void run_contract(const eb_contract_desc* d, void* ws, size_t ws_bytes, cudaStre
   prm.G = p.G;
   prm.segmax = p.segmax;
   prm.R = (int)d->R;
+  prm.outer = d->P;
   prm.pre = to_list(d->n_pre, d->pre);
   prm.mid = to_list(p.col ? 0 : d->n_mid, d->mid);
   if (sc) {

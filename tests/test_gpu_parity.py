@@ -93,7 +93,10 @@ def test_contract_mttkrp_order3(eb, I, J, K, R, mode, fused_tma, opts):
 
 
 @pytest.mark.parametrize("I,J,K,B", [(5, 40, 34, 64), (3, 70, 130, 16), (4, 33, 64, 24),
-                                     (2, 9, 2, 100), (1, 256, 258, 8)])
+                                     (2, 9, 2, 100), (1, 256, 258, 8),
+                                     # narrow M (K here): OS outer indices per tile
+                                     (37, 64, 16, 64), (8, 100, 16, 24), (13, 40, 24, 16),
+                                     (16, 32, 32, 64), (9, 20, 12, 8)])
 @pytest.mark.parametrize("fused_tma", [True, False])
 def test_contract_ttm(eb, I, J, K, B, fused_tma, opts):
     from paper_2206_08301_b200 import _capi as C
