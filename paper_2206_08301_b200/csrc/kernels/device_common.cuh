@@ -136,6 +136,7 @@ inline ScatterDiv make_scatter_div(const eb_scatter& s) {
 __device__ __forceinline__ void scatter_part(const eb_scatter& s, const ScatterDiv& v, int d0,
                                              int d1, int64_t x, int64_t& rank, int64_t& off) {
   uint32_t r = (uint32_t)x;
+#pragma unroll 1
   for (int d = d1 - 1; d >= d0; --d) {
     const uint32_t q = fdiv(r, v.ext[d]);
     const uint32_t xd = r - q * v.ext[d].d;
@@ -149,6 +150,7 @@ __device__ __forceinline__ void scatter_part(const eb_scatter& s, const ScatterD
 
 __device__ __forceinline__ void scatter_store(const eb_scatter& s, int64_t rank, int64_t off,
                                               double v) {
+#pragma unroll 1
   for (int k = 0; k < s.n_rep; ++k) s.dest[rank + s.rep_offset[k]][off] = v;
 }
 
@@ -211,6 +213,7 @@ __device__ __forceinline__ void scatter_pair(const eb_scatter& s, int64_t rank, 
   const int64_t o0 = off + c0.off, o1 = off + c1.off;
   const int64_t r0 = rank + c0.rank, r1 = rank + c1.rank;
   if (has1 && r0 == r1 && o1 == o0 + 1 && (o0 & 1) == 0) {
+#pragma unroll 1
     for (int k = 0; k < s.n_rep; ++k)
       *reinterpret_cast<double2*>(s.dest[r0 + s.rep_offset[k]] + o0) = make_double2(v0, v1);
     return;

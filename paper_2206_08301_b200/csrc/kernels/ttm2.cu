@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
       scatter_part(s, v, 0, s.n_outer, p, ro, oo);
       const int dr = s.n_outer, dc = s.n_outer + s.n_row;
       const RowBase rb = scatter_rowbase(s, v, dr, dc, r0, kRows, ro, oo);
-#pragma unroll
+#pragma unroll 1
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
         if (r < prm.M) {
