@@ -83,6 +83,9 @@ struct Ttm2Params {
   double* out;
   eb_scatter sc;  // sc.nd > 0: scatter epilogue (the next term's blocks, not `out`)
   ScatterDiv scd;
+  // the (b, c) tail lands unsplit and row-major in every destination block:
+  // an item whose rows stay in one block is one strided tile store
+  int fast_tail;
 };
 
 template <int NW>
@@ -551,6 +554,39 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
       scatter_part(s, v, 0, s.n_outer, p, ro, oo);
       const int dr = s.n_outer, dc = s.n_outer + s.n_row;
       const RowBase rb = scatter_rowbase(s, v, dr, dc, r0, kRows, ro, oo);
+      if (prm.fast_tail && rb.linear) {
+        // one destination block for the whole item, (b, c) row-major in it:
+        // the plain epilogue with another base and row stride
+#pragma unroll
+        for (int ri = 0; ri < RW; ++ri) {
+          const int64_t r = r0 + RW * w1 + ri;
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const int64_t b = 8 * mi + g;
+            if (r < prm.M && b < prm.N1) {
+              const int64_t off = rb.off + (int64_t)(RW * w1 + ri) * rb.step + b * prm.N2;
+#pragma unroll 1
+              for (int k = 0; k < s.n_rep; ++k) {
+                double* dst = s.dest[rb.rank + s.rep_offset[k]] + off;
+#pragma unroll
+                for (int nj = 0; nj < 2; ++nj) {
+                  const int64_t c = 8 * nj + 2 * l;
+                  if (c + 1 < prm.N2 && (reinterpret_cast<uintptr_t>(dst + c) & 15) == 0) {
+                    *reinterpret_cast<double2*>(dst + c) =
+                        make_double2(acc[ri][mi][nj][0], acc[ri][mi][nj][1]);
+                  } else {
+                    if (c < prm.N2) dst[c] = acc[ri][mi][nj][0];
+                    if (c + 1 < prm.N2) dst[c + 1] = acc[ri][mi][nj][1];
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int nj = 0; nj < 2; ++nj) acc[ri][mi][nj][0] = acc[ri][mi][nj][1] = 0.0;
+          }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
@@ -646,6 +682,14 @@ void run_ttm2(const eb_ttm2_desc* d, cudaStream_t st, const eb_scatter* sc = nul
   if (sc) {
     prm.sc = *sc;
     prm.scd = make_scatter_div(*sc);
+    // tail (b, c) = the last two natural dims: whole (unsplit) and row-major
+    // (c contiguous, b stride N2) in the destination blocks
+    const int b = sc->nd - 2, c = sc->nd - 1;
+    bool whole = sc->nd >= 3 && sc->n_outer + sc->n_row == sc->nd - 2;
+    for (int dd : {b, c})
+      whole = whole && sc->ext[dd] == d->N1 * (dd == b) + d->N2 * (dd == c) &&
+              sc->gbase[dd] % sc->block[dd] + sc->ext[dd] <= sc->block[dd];
+    prm.fast_tail = whole && sc->local_stride[c] == 1 && sc->local_stride[b] == d->N2 ? 1 : 0;
   }
   prm.P = d->P;
   prm.Q1 = d->Q1;

@@ -51,6 +51,9 @@ def time_runs(ex, st, reps=5):
 def main():
     out = []
     cases = [("C4", P) for P in (2, 4, 8)] + [("C5", 4)]
+    if os.environ.get("PUSH_AB_ONLY"):  # e.g. "C5:4"
+        n, p = os.environ["PUSH_AB_ONLY"].split(":")
+        cases = [(n, int(p))]
     for name, P in cases:
         c = CONFIGS[name]
         e, ext = c["einsums"][0], c["extents"](P)
@@ -83,7 +86,7 @@ def main():
         ex.close()
         torch.cuda.empty_cache()
     eb.set_option("fuse_redistribution", 1)
-    if len(sys.argv) > 1:
+    if len(sys.argv) > 1 and not os.environ.get("PUSH_AB_ONLY"):
         with open(sys.argv[1], "w") as f:
             for r in out:
                 f.write(json.dumps(r) + "\n")
