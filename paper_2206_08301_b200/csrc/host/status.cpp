@@ -47,6 +47,8 @@ Options read_env() {
   if (const char* v = std::getenv("EB_CHAIN_TERMS")) o.chain_terms = v[0] != '0';
   if (const char* v = std::getenv("EB_CHAIN_FLAGS")) o.chain_flags = std::atoi(v);
   if (const char* v = std::getenv("EB_CHAIN_LAG")) o.chain_lag = std::atoi(v);
+  if (const char* v = std::getenv("EB_PDL")) o.pdl = v[0] != '0';
+  if (const char* v = std::getenv("EB_SCATTER_FAST")) o.scatter_fast = v[0] != '0';
   return o;
 }
 

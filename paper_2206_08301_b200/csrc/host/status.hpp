@@ -76,6 +76,8 @@ struct Options {
   int chain_terms = 0;
   int chain_flags = 7;    // eb_ttm2_chain cache policy bits (ttm2.cu ChainParams::flags)
   int chain_lag = 1;      // eb_ttm2_chain: term B of slab p runs in group p + lag
+  int pdl = 1;            // programmatic dependent launch for the chained kernels
+  int scatter_fast = 1;   // ttm2 scatter: single-block fast tail path
 };
 const Options& options();
 
