@@ -1195,7 +1195,8 @@ void ScheduleExecutor::arm_push() {
         fail(errc::invalid_argument, "push: destination heap not mapped");
       b.ptr = reinterpret_cast<double*>(base + off);
     } else if (transport_->owns(r)) {
-      b.ptr = run_arena_.alloc(prod(b.shape), stream_, false);
+      // (option zero_push: zeroed first, so a missing store shows in the result)
+      b.ptr = run_arena_.alloc(prod(b.shape), stream_, eb::options().zero_push != 0);
     }
   }
 }

@@ -49,6 +49,7 @@ Options read_env() {
   if (const char* v = std::getenv("EB_CHAIN_LAG")) o.chain_lag = std::atoi(v);
   if (const char* v = std::getenv("EB_PDL")) o.pdl = v[0] != '0';
   if (const char* v = std::getenv("EB_SCATTER_FAST")) o.scatter_fast = v[0] != '0';
+  if (const char* v = std::getenv("EB_ZERO_PUSH")) o.zero_push = v[0] != '0';
   return o;
 }
 
@@ -114,6 +115,12 @@ extern "C" int eb_set_option(const char* name, const char* value) {
       o.ttm2_variant = v;
     } else if (!std::strcmp(name, "fuse_ttm2")) {
       o.fuse_ttm2 = v != 0;
+    } else if (!std::strcmp(name, "zero_push")) {
+      o.zero_push = v != 0;
+    } else if (!std::strcmp(name, "scatter_fast")) {
+      o.scatter_fast = v != 0;
+    } else if (!std::strcmp(name, "pdl")) {
+      o.pdl = v != 0;
     } else if (!std::strcmp(name, "chain_terms")) {
       o.chain_terms = v != 0;
     } else if (!std::strcmp(name, "fuse_redistribution")) {

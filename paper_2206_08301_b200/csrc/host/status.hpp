@@ -78,6 +78,7 @@ struct Options {
   int chain_lag = 1;      // eb_ttm2_chain: term B of slab p runs in group p + lag
   int pdl = 1;            // programmatic dependent launch for the chained kernels
   int scatter_fast = 1;   // ttm2 scatter: single-block fast tail path
+  int zero_push = 0;      // zero the pushed destination blocks first (tests: missing stores)
 };
 const Options& options();
 

@@ -325,16 +325,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 // j halves summed by step 1), 1 -> 4 step-0 warps each contracting all 64 j
 // (one step-0 and one step-1 warp per sub-partition, fewer non-DMMA
 // instructions per stage).
-// SC (scatter epilogue): same ring depths.  (A 4-deep t0 ring for the
-// scatter variant measured 0.1 ms faster on C5 P = 4 but produced one wrong
-// 16-row tile in ~1 of 4 batches of back-to-back runs — tools/c5p4_det2.py;
-// cause not found, so the shipped variant keeps the 2-deep ring, which ran
-// 0 wrong batches in 32.)
+// SC (scatter epilogue): the step-1 warps spend longer per item between
+// their t0 slices, so the t0 ring is 4 deep where shared memory allows
+// (JP = 1) and step 0 keeps streaming meanwhile.
 template <int JP, bool SC = false>
 struct WsCfg {
   static constexpr int S0 = 4 * JP, S1 = 4, Warps = S0 + S1 + 1;
   static constexpr int JW = kJ / JP, B16 = JW / 16;
-  static constexpr int Stages = 6, T0Slots = 2;
+  static constexpr int Stages = 6, T0Slots = (SC && JP == 1) ? 4 : 2;
   static constexpr int T0Bytes = JP * kK * kPlane;  // [j part][k][16 r][16 b]
   static constexpr int Smem = Stages * kXBytes + T0Slots * T0Bytes + 1024;
 };
@@ -589,7 +587,9 @@ __global__ void __launch_bounds__(WsCfg<JP>::Warps * 32, 1)
         }
         continue;
       }
-#pragma unroll 1
+      // (fully unrolled: acc[ri] must stay a register array — a rolled loop
+      // indexing it dynamically lost stores in the JP = 2 variant)
+#pragma unroll
       for (int ri = 0; ri < RW; ++ri) {
         const int64_t r = r0 + RW * w1 + ri;
         if (r < prm.M) {

@@ -984,20 +984,31 @@ def test_ttm2_chain_both_terms_one_launch(eb, P, ext, opts):
 
 @pytest.mark.parametrize("e,ext,P", [
     ("ijklm,jb,kc,ld,me->ibcde", dict(i=128, j=32, k=32, l=32, m=32, b=16, c=16, d=16, e=16), 4),
+    ("ijklm,jb,kc,ld,me->ibcde", dict(i=256, j=32, k=32, l=32, m=32, b=16, c=16, d=16, e=16), 4),
     ("ijk,jb,kc->ibc", dict(i=256, j=256, k=256, b=64, c=64), 8),
 ])
-def test_back_to_back_runs_are_bitwise_stable(eb, e, ext, P):
+@pytest.mark.parametrize("variant", [1, 2])
+def test_back_to_back_runs_are_bitwise_stable(eb, e, ext, P, variant, opts):
     """Batches of back-to-back runs with no host sync in between (the bench
     pattern: launches overlap under programmatic dependent launch, blocks are
     recycled by the stream-ordered pool) give bitwise the output of a single
-    synchronised run — catches ordering races in the fused redistribution."""
+    synchronised run, with the pushed destination blocks zeroed before every
+    run (so a store the scatter epilogue misses cannot hide behind the
+    previous run's identical data), for both ttm2 step-0 splits."""
     import torch
+    opts("zero_push", 1)
+    opts("ttm2_variant", variant)
     ops = oracle.seeded_inputs(e, ext, 81)
+    if e.startswith("ijklm"):
+        want = _ttmc_o5_chain(ext, ops)
+    else:
+        want = oracle.naive_evaluate(e, ext, ops)
     ex = eb.Executor(e, ext, P)
     ex.stage(ops)
     ex.run()
     torch.cuda.synchronize()
     ref = ex.gather().copy()
+    check(ref, want)
     assert ex.stats()["fused_redistributions"] == 1
     for _ in range(6):
         for _ in range(5):
