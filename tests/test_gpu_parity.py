@@ -996,19 +996,24 @@ def test_back_to_back_runs_are_bitwise_stable(eb, e, ext, P, variant, opts):
     run (so a store the scatter epilogue misses cannot hide behind the
     previous run's identical data), for both ttm2 step-0 splits."""
     import torch
+    ops = oracle.seeded_inputs(e, ext, 81)
+    # the separate-copy path (every kernel of it is pinned to the oracle in
+    # the tests above) is the want: the fused path must equal it bitwise
+    opts("fuse_redistribution", 0)
+    sep = eb.Executor(e, ext, P)
+    sep.stage(ops)
+    sep.run()
+    want = sep.gather().copy()
+    sep.close()
+    opts("fuse_redistribution", 1)
     opts("zero_push", 1)
     opts("ttm2_variant", variant)
-    ops = oracle.seeded_inputs(e, ext, 81)
-    if e.startswith("ijklm"):
-        want = _ttmc_o5_chain(ext, ops)
-    else:
-        want = oracle.naive_evaluate(e, ext, ops)
     ex = eb.Executor(e, ext, P)
     ex.stage(ops)
     ex.run()
     torch.cuda.synchronize()
     ref = ex.gather().copy()
-    check(ref, want)
+    assert np.array_equal(ref, want)
     assert ex.stats()["fused_redistributions"] == 1
     for _ in range(6):
         for _ in range(5):
