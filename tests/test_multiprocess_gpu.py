@@ -63,6 +63,8 @@ def _virtual(eb, e, ext, procs, ops):
 @pytest.mark.parametrize("case,procs", [
     ("mttkrp_m0", 2), ("mttkrp_m0", 4), ("mttkrp_m2", 4),
     ("ttmc3", 2), ("ttmc3", 4), ("ttmc5", 4), ("2mm", 4), ("3mm", 4),
+    # eight real processes: depth-4 groups, the pushed TTMc exchanges
+    ("mttkrp_m0", 8), ("ttmc3", 8), ("ttmc5", 8), ("2mm", 8),
 ])
 def test_peer_processes_match_oracle_and_virtual(eb, case, procs, tmp_path):
     e, ext, seed = CASES[case]
