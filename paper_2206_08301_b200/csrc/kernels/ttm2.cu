@@ -884,8 +884,9 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
         // a sleeping poll: this warp shares an SM sub-partition with
         // DMMA-saturated warps, a spinning one would steal their issue slots
         while (!mbar_try_wait(smem_addr(&rel_full[s]), (na / kRel) & 1)) __nanosleep(200);
+        // release-only publication (a full __threadfence also invalidates
+        // the SM's L1 — the step-1 warps' factor loads — every tile)
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(prm.done + p) : "memory");
         mbar_arrive(smem_addr(&rel_empty[s]));
         ++na;
