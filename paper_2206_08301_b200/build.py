@@ -16,8 +16,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build", "obj")
-LIB = os.path.join(PKG, "lib", "libeinplan_b200.so")
+# EB_BUILD_TAG=t + EB_BUILD_DEFS="-DX ..." build an A/B variant of the
+# library (build/obj_t, lib/t/libeinplan_b200.so; load it with EB_LIB_PATH).
+_TAG = os.environ.get("EB_BUILD_TAG", "")
+_DEFS = os.environ.get("EB_BUILD_DEFS", "").split()
+OBJ = os.path.join(PKG, "build", "obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, "lib", *([_TAG] if _TAG else []), "libeinplan_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NCCL_ROOT = None
@@ -58,7 +62,7 @@ def _compile(src: str, hdr_time: float, nccl: str | None) -> str:
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_time):
         return obj
     inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-isystem", _nlohmann()]
-    defs = []
+    defs = list(_DEFS)
     if nccl:
         inc.append("-I" + os.path.join(nccl, "include"))
         defs.append("-DEB_HAVE_NCCL=1")
