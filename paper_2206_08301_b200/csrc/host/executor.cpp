@@ -1693,9 +1693,9 @@ namespace {
 //   EINPLAN_EXEC      "virtual" forces every rank onto the current device;
 //   EINPLAN_DEVICES   "d0,d1,..." explicit rank -> device map (cycled), e.g.
 //                     "0,0" runs two rank threads on one GPU (peer transport);
-//   EINPLAN_TRANSPORT "nccl" | "peer" for the one-thread-per-GPU mode.
+//   EINPLAN_TRANSPORT "nccl" | "hybrid" | "peer" for the one-thread-per-GPU mode.
 // Default: one host thread per GPU on devices 0..procs-1 when procs <= the
-// visible GPU count (NCCL when the devices are distinct), else virtual ranks.
+// visible GPU count (hybrid when the devices are distinct), else virtual ranks.
 struct ExecChoice {
   bool threads = false;
   std::vector<int> dev;
