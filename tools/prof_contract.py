@@ -4,7 +4,8 @@ or timed A/B variants with CUDA events.
 usage: python tools/prof_contract.py CFG [REPS] [ENV=VAL,... ...]
   CFG in c1, c2m0, c2m1, c2m2, c2pair (eb_mttkrp2: modes 0+1 in one pass), c3,
   p8m0/p8m1/p8m2 (C2's per-GPU 512^3 block at P = 8).  With variant args, the variants are run
-  round-robin (3 rounds) and the best ms / TFLOP/s of each is printed.
+  round-robin (3 rounds) and the best ms / TFLOP/s of each is printed; a variant is
+  NAME=VAL,... where lower-case names are eb_set_option options (e.g. row_tile=1).
 """
 import ctypes
 import json
@@ -96,8 +97,11 @@ res = {}
 for rnd in range(3):
     for v in variants:
         kv = [x.split("=") for x in v.split(",") if x]
-        for k, val in kv:
-            os.environ[k] = val
+        for k, val in kv:  # lower-case names are eb_set_option options
+            if k.islower():
+                C.check(L.eb_set_option(k.encode(), val.encode()))
+            else:
+                os.environ[k] = val
         launch(); launch()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
