@@ -302,6 +302,15 @@ int eb_exec_run(eb_exec* h);
  * default: every operation is then ordered on `stream`. */
 int eb_exec_set_async_reduce(eb_exec* h, int on);
 int eb_exec_join(eb_exec* h);
+/* CUDA graph of one run (virtual or NCCL transport): eb_exec_capture runs
+ * once eagerly (every block of the run then keeps its address), captures a
+ * second run on the executor's stream and instantiates it; eb_exec_replay
+ * launches the graph — the same kernels, copies and collectives, one host
+ * call.  Re-staging inputs keeps the graph valid; capture again after
+ * changing options or shared inputs.  EB_E_INVALID for the peer / hybrid
+ * transports or the legacy default stream. */
+int eb_exec_capture(eb_exec* h);
+int eb_exec_replay(eb_exec* h);
 /* CP sweep dimension tree: run `mode0` (ijk,ja,ka->ia) and `mode1`
  * (ijk,ia,ka->ja, X and the k factor shared from mode0 with
  * eb_exec_share_input, same grid, same stream) in one pass over X with

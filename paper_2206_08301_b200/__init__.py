@@ -29,6 +29,7 @@ from . import _capi
 from ._capi import EinplanError
 
 __all__ = ["Session", "Executor", "EinplanError", "RandomStream", "bench_json", "plan_json",
+           "launch_count",
            "random_tensor", "set_option", "version", "dims_string"]
 
 
@@ -142,6 +143,12 @@ class RandomStream:
             self.close()
         except Exception:
             pass
+
+
+def launch_count() -> int:
+    """Kernel launches issued by the library so far (graph replays add the
+    launches of their captured run)."""
+    return int(_capi.lib().eb_launch_count())
 
 
 def mem_in_use() -> int:
@@ -343,6 +350,15 @@ class Executor:
     def join(self):
         """Order the compute stream after this executor's pending reduction."""
         _capi.check(_capi.lib().eb_exec_join(self._h))
+
+    def capture(self):
+        """Capture one run as a CUDA graph (after a warm eager run); then
+        :meth:`replay` launches it.  Virtual / NCCL transports only."""
+        _capi.check(_capi.lib().eb_exec_capture(self._h))
+
+    def replay(self):
+        """Launch the captured run (same kernels and collectives, one host call)."""
+        _capi.check(_capi.lib().eb_exec_replay(self._h))
 
     def run_pair(self, mode1: "Executor") -> bool:
         """CP-sweep dimension tree: this executor (order-3 mode 0) and ``mode1``

@@ -65,7 +65,7 @@ EXPORTS = [
     "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
-    "eb_exec_join", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
+    "eb_exec_join", "eb_exec_capture", "eb_exec_replay", "eb_exec_gather", "eb_exec_output_elems", "eb_exec_stats",
     "eb_exec_report_json", "eb_launch_count", "eb_timer_enable", "eb_timer_collect",
 ]
 
@@ -129,6 +129,8 @@ def lib():
         _sig(L, "eb_exec_run_pair", ctypes.c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_int)])
         _sig(L, "eb_exec_set_async_reduce", ctypes.c_int, [_vp, ctypes.c_int])
         _sig(L, "eb_exec_join", ctypes.c_int, [_vp])
+        _sig(L, "eb_exec_capture", ctypes.c_int, [_vp])
+        _sig(L, "eb_exec_replay", ctypes.c_int, [_vp])
         _sig(L, "eb_random_fill_host", None, [_dp, _i64, ctypes.c_uint64, _i64])
         _sig(L, "eb_random_fill_block", ctypes.c_int,
              [_dp, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),

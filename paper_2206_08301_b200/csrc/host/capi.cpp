@@ -566,6 +566,20 @@ int eb_exec_join(eb_exec* h) {
   });
 }
 
+int eb_exec_capture(eb_exec* h) {
+  return exec_guard([&] {
+    if (!h) throw eb::InvalidError("eb_exec_capture: null handle");
+    h->exec->capture();
+  });
+}
+
+int eb_exec_replay(eb_exec* h) {
+  return exec_guard([&] {
+    if (!h) throw eb::InvalidError("eb_exec_replay: null handle");
+    h->exec->replay();
+  });
+}
+
 int eb_exec_run_pair(eb_exec* mode0, eb_exec* mode1, int* fused) {
   return exec_guard([&] {
     if (!mode0 || !mode1) throw eb::InvalidError("eb_exec_run_pair: null handle");

@@ -114,19 +114,40 @@ void copy_box_host(bool h2d, double* host, const std::vector<std::int64_t>& gsha
 double* DeviceArena::alloc(std::int64_t elems, cudaStream_t st, bool zero) {
   void* p = nullptr;
   const std::size_t bytes = static_cast<std::size_t>(std::max<std::int64_t>(elems, 1)) * 8;
-  cuda_ok(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+  for (std::size_t i = 0; recycle_ && i < kept_.size(); ++i)
+    if (kept_[i].first == bytes) {
+      p = kept_[i].second;
+      kept_.erase(kept_.begin() + static_cast<std::ptrdiff_t>(i));
+      break;
+    }
+  if (!p) {
+    cuda_ok(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+    ++mallocs_;
+  }
   if (zero) cuda_ok(cudaMemsetAsync(p, 0, bytes, st), "cudaMemsetAsync");
-  live_.push_back(p);
+  live_.emplace_back(bytes, p);
   return static_cast<double*>(p);
 }
 
 void DeviceArena::release(cudaStream_t st) {
-  for (void* p : live_) cudaFreeAsync(p, st);
+  if (recycle_) {
+    kept_.insert(kept_.end(), live_.begin(), live_.end());
+  } else {
+    for (auto& b : live_) cudaFreeAsync(b.second, st);
+  }
   live_.clear();
 }
 
+void DeviceArena::set_recycle(bool on, cudaStream_t st) {
+  if (!on)
+    for (auto& b : kept_) cudaFreeAsync(b.second, st);
+  if (!on) kept_.clear();
+  recycle_ = on;
+}
+
 DeviceArena::~DeviceArena() {
-  for (void* p : live_) cudaFree(p);
+  for (auto& b : live_) cudaFree(b.second);
+  for (auto& b : kept_) cudaFree(b.second);
 }
 
 // ------------------------------------------------------- transports --
@@ -488,7 +509,9 @@ ScheduleExecutor::~ScheduleExecutor() {
   cudaStreamSynchronize(stream_);
   if (ev_compute_) cudaEventDestroy(ev_compute_);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   run_arena_.release(stream_);
+  run_arena_.set_recycle(false, stream_);
   input_arena_.release(stream_);
   cudaFreeAsync(workspace_, stream_);
   cudaStreamSynchronize(stream_);
@@ -1342,6 +1365,59 @@ void ScheduleExecutor::join() {
   if (!comm_pending_) return;
   cuda_ok(cudaStreamWaitEvent(stream_, ev_comm_, 0), "join: wait for the reduction");
   comm_pending_ = false;
+}
+
+void ScheduleExecutor::capture() {
+  if (transport_->peer_mapped())
+    fail(errc::invalid_argument,
+         "capture: the peer transport meets its peers on the host between kernels; "
+         "graphs need the virtual or NCCL transport");
+  if (stream_ == nullptr || stream_ == cudaStreamLegacy || stream_ == cudaStreamPerThread)
+    fail(errc::invalid_argument, "capture: needs an explicitly created stream");
+  if (graph_exec_) {
+    cuda_ok(cudaGraphExecDestroy(graph_exec_), "graph destroy");
+    graph_exec_ = nullptr;
+  }
+  // warm run: the recycling arena keeps every block of the run, the
+  // workspace and the transport's buffers reach their final sizes
+  run_arena_.set_recycle(true, stream_);
+  execute();
+  join();
+  cuda_ok(cudaStreamSynchronize(stream_), "capture: warm run");
+  const long long mallocs0 = run_arena_.mallocs();
+  const std::size_t ws0 = workspace_bytes_;
+  const long long n0 = eb_launch_count();
+  eb::set_capturing(true);
+  cuda_ok(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  cudaGraph_t g = nullptr;
+  try {
+    execute();
+    join();
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    eb::set_capturing(false);
+    throw;
+  }
+  const cudaError_t e = cudaStreamEndCapture(stream_, &g);
+  eb::set_capturing(false);
+  cuda_ok(e, "end capture");
+  graph_launches_ = eb_launch_count() - n0;
+  if (run_arena_.mallocs() != mallocs0 || workspace_bytes_ != ws0) {
+    cudaGraphDestroy(g);
+    fail(errc::invalid_argument, "capture: the captured run allocated memory (blocks differ "
+                                 "from the warm run)");
+  }
+  const cudaError_t ie = cudaGraphInstantiateWithFlags(&graph_exec_, g, 0);
+  cudaGraphDestroy(g);
+  cuda_ok(ie, "graph instantiate");
+}
+
+void ScheduleExecutor::replay() {
+  if (!graph_exec_) fail(errc::invalid_argument, "replay: no captured run (call capture)");
+  join();
+  cuda_ok(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
+  eb::count_launches(graph_launches_);
 }
 
 std::int64_t ScheduleExecutor::reduce(const TensorPlacement& place, const ReductionGroup& grp,

@@ -36,9 +36,16 @@ class DeviceArena {
   ~DeviceArena();
   double* alloc(std::int64_t elems, cudaStream_t st, bool zero);
   void release(cudaStream_t st);
+  // Recycling: release() keeps the blocks and alloc() hands back a kept
+  // block of the same size before allocating — a captured CUDA graph then
+  // replays on fixed addresses (and a run allocates nothing).
+  void set_recycle(bool on, cudaStream_t st);
+  long long mallocs() const { return mallocs_; }
 
  private:
-  std::vector<void*> live_;
+  std::vector<std::pair<std::size_t, void*>> live_, kept_;
+  bool recycle_ = false;
+  long long mallocs_ = 0;
 };
 
 // How ranks exchange data: all virtual ranks on one device; one rank per
@@ -200,6 +207,16 @@ class ScheduleExecutor {
   // of the same schedule, gather() and the next execute() join implicitly.
   void set_async_reduce(bool on) { async_reduce_ = on; }
   void join();
+  // CUDA graph of one run: execute() once eagerly (the run arena switches
+  // to recycling, so every block of the run keeps its address), then
+  // capture a second execute() on the executor's stream and instantiate it.
+  // replay() launches that graph: the same kernels, copies and collectives
+  // with one host call.  Virtual and NCCL transports (the peer transport
+  // meets its peers on the host between kernels); re-staging inputs keeps
+  // the graph valid (input blocks never move).
+  void capture();
+  void replay();
+  bool captured() const { return graph_exec_ != nullptr; }
   // Canonical output blocks to host (virtual, or rank 0 over NCCL).
   void gather(double* host_out);
   void verify(const std::vector<const double*>& global_inputs, const double* host_out,
@@ -281,6 +298,8 @@ class ScheduleExecutor {
   int redistributions_fused_ = 0;
   bool async_reduce_ = false, comm_pending_ = false;
   cudaEvent_t ev_compute_ = nullptr, ev_comm_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  long long graph_launches_ = 0;  // kernel launches inside the captured run
   // exchange heap (PeerTransport only)
   char* heap_ = nullptr;
   std::size_t heap_bytes_ = 0;

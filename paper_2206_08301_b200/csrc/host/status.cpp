@@ -30,6 +30,7 @@ std::atomic<bool> g_timing{false};
 std::mutex g_mu;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 thread_local cudaEvent_t g_open = nullptr;  // one open bracket per launching thread
+thread_local bool g_capturing = false;
 
 Options read_env() {
   Options o;
@@ -70,16 +71,18 @@ void set_smem_attr_once(const void* kernel, int bytes) {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_capturing(bool on) { g_capturing = on; }
 
 void main_kernel_begin(cudaStream_t st) {
-  if (!g_timing.load()) return;
+  if (!g_timing.load() || g_capturing) return;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEventCreate(&g_open);
   cudaEventRecord(g_open, st);
 }
 
 void main_kernel_end(cudaStream_t st) {
-  if (!g_timing.load()) return;
+  if (!g_timing.load() || g_capturing) return;
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_open) return;
   cudaEvent_t e = nullptr;

@@ -54,6 +54,10 @@ namespace eb {
 // the dominant contraction kernel can additionally be bracketed by CUDA
 // events on its own stream (bench.py's live roofline timing).
 void count_launch();
+void count_launches(long long n);  // a CUDA-graph replay of n captured launches
+// While this thread captures a CUDA graph the main-kernel events are skipped
+// (they would become graph nodes).
+void set_capturing(bool on);
 void main_kernel_begin(cudaStream_t st);
 void main_kernel_end(cudaStream_t st);
 
