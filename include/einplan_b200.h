@@ -152,6 +152,20 @@ size_t eb_ttm2_chain_workspace(const eb_ttm2_desc* a);
 int eb_ttm2_chain(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* Both TTMc-O5 terms with term B's second contraction folded into term A
+ * (same hand-over condition as eb_ttm2_chain): term B's last mode m (Q2b,
+ * a multiple of 16, <= 64) is the innermost mode of term A's rows, so
+ *   s[p][R'][e][b c]  = sum_m t1[p][R'][m][b c] U2b[m][e]   (term A's epilogue)
+ *   b->out[q][b c][d][e] = sum_l U1b[l][d] s[q][l][e][b c]   (a second kernel)
+ * and t1 is never stored.  Reference: the two terms of the schedule
+ * (executor.cpp:220-235) with the self hand-over (redistribute.cpp:185-206);
+ * equal to it up to the summation order of l and m.  a->out and b->X are
+ * ignored; workspace = eb_ttmc_fold_workspace(a, b) bytes (s).  Needs the
+ * eb_ttm2 limits on both terms and N1b, N2b <= 16. */
+size_t eb_ttmc_fold_workspace(const eb_ttm2_desc* a, const eb_ttm2_desc* b);
+int eb_ttmc_fold(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
 /* eb_contract (EB_COL, EB_BATCHED only) / eb_ttm2 with the scatter epilogue;
  * d->out is ignored. */
 int eb_contract_scatter(const eb_contract_desc* d, const eb_scatter* s, void* workspace,
@@ -239,7 +253,8 @@ int eb_plan_json(const char* einsum, const char* dims, int64_t procs, double fas
  * (row tile, 64-column block) items instead of per-64-column split-K),
  * "fuse_redistribution" 0/1 (TTM outputs pushed by the producing kernel into
  * the next term's blocks, eb_scatter), "chain_terms" 0/1 (two TTM-pair
- * terms joined by a self hand-over in one eb_ttm2_chain launch). */
+ * terms joined by a self hand-over in one eb_ttm2_chain launch), "fold_terms"
+ * 0/1 (such terms as eb_ttmc_fold, t1 never stored; default 0). */
 int eb_set_option(const char* name, const char* value);
 
 /* ---- rank-local executor (the GPU run(), executor.cpp:156-263) ----------

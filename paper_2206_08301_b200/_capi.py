@@ -61,7 +61,7 @@ EXPORTS = [
     "eb_group_sum", "eb_group_sum_into", "eb_copy_box", "eb_set_option", "eb_exec_create_peer",
     "eb_exec_stage_region", "eb_rng_create", "eb_rng_fill", "eb_rng_destroy", "eb_mem_in_use", "eb_pad_rows", "eb_permute",
     "eb_contract_scatter", "eb_ttm2_scatter", "eb_exec_fused_redistributions",
-    "eb_ttm2_chain", "eb_ttm2_chain_workspace", "eb_exec_create_hybrid", "eb_einsum_generic", "eb_random_fill_host",
+    "eb_ttm2_chain", "eb_ttm2_chain_workspace", "eb_ttmc_fold", "eb_ttmc_fold_workspace", "eb_exec_create_hybrid", "eb_einsum_generic", "eb_random_fill_host",
     "eb_random_fill_block", "eb_exec_block", "eb_exec_stage_block", "eb_free",
     "eb_plan_json", "eb_nccl_unique_id", "eb_exec_create", "eb_exec_create_like", "eb_exec_destroy", "eb_exec_stage",
     "eb_exec_share_input", "eb_exec_run", "eb_exec_run_pair", "eb_exec_set_async_reduce",
@@ -161,6 +161,10 @@ def lib():
         _sig(L, "eb_ttm2_scatter", ctypes.c_int, [ctypes.POINTER(Ttm2Desc), _vp, _vp])
         _sig(L, "eb_ttm2_chain_workspace", ctypes.c_size_t, [ctypes.POINTER(Ttm2Desc)])
         _sig(L, "eb_ttm2_chain", ctypes.c_int,
+             [ctypes.POINTER(Ttm2Desc), ctypes.POINTER(Ttm2Desc), _vp, ctypes.c_size_t, _vp])
+        _sig(L, "eb_ttmc_fold_workspace", ctypes.c_size_t,
+             [ctypes.POINTER(Ttm2Desc), ctypes.POINTER(Ttm2Desc)])
+        _sig(L, "eb_ttmc_fold", ctypes.c_int,
              [ctypes.POINTER(Ttm2Desc), ctypes.POINTER(Ttm2Desc), _vp, ctypes.c_size_t, _vp])
         _sig(L, "eb_free", None, [_vp])
         _sig(L, "eb_plan_json", ctypes.c_int,

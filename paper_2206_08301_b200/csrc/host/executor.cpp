@@ -1023,7 +1023,8 @@ bool ScheduleExecutor::try_fused_ttm2(const TermPlan& term, std::int64_t rank,
 }
 
 const TermPlan* ScheduleExecutor::chain_next(const TermPlan& a) const {
-  if (!eb::options().fuse_ttm2 || !eb::options().chain_terms || a.reduction.depth > 1)
+  const bool chain = eb::options().chain_terms != 0;
+  if (!eb::options().fuse_ttm2 || !(chain || eb::options().fold_terms) || a.reduction.depth > 1)
     return nullptr;
   const TermPlan* b = nullptr;
   for (const TermPlan& t : pipe_.schedule.terms)
@@ -1048,8 +1049,16 @@ const TermPlan* ScheduleExecutor::chain_next(const TermPlan& a) const {
     if (b0.lhs_indices != na || pipe_.tree.tensor_name(b0.lhs) != a.statement.output)
       return nullptr;
     if (da.P != db.P || db.Q1 * db.Q2 * db.M != da.M * da.N1 * da.N2) return nullptr;
+    if (!chain && !fold_shape(da, db)) return nullptr;
   }
   return b;
+}
+
+// eb_ttmc_fold: term B's second contraction (mode m, Q2b) is the innermost
+// mode of term A's rows and term B's rows are term A's (b, c) (ttmc_fold.cu)
+bool ScheduleExecutor::fold_shape(const eb_ttm2_desc& da, const eb_ttm2_desc& db) {
+  return db.Q2 % 16 == 0 && db.Q2 <= 64 && da.M % db.Q2 == 0 && db.M == da.N1 * da.N2 &&
+         db.N1 <= 16 && db.N2 <= 16;
 }
 
 void ScheduleExecutor::run_chain(const TermPlan& a, const TermPlan& b, std::int64_t rank,
@@ -1090,6 +1099,13 @@ void ScheduleExecutor::run_chain(const TermPlan& a, const TermPlan& b, std::int6
   db.U2 = u4.ptr;
   db.ldu2 = u4.shape[1];
   db.out = out.ptr;
+  if (!eb::options().chain_terms) {  // fold: t1 (the block above) is never written
+    const std::size_t fb = eb_ttmc_fold_workspace(&da, &db);
+    eb_ok(eb_ttmc_fold(&da, &db, workspace(fb), fb, stream_),
+          "eb_ttmc_fold (both TTMc terms, m folded into term A)");
+    launches_fused_ += 2;
+    return;
+  }
   const std::size_t wb = eb_ttm2_chain_workspace(&da);
   eb_ok(eb_ttm2_chain(&da, &db, workspace(wb), wb, stream_), "eb_ttm2_chain (both TTMc terms)");
   ++launches_fused_;

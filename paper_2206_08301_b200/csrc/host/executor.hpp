@@ -263,6 +263,7 @@ class ScheduleExecutor {
   // whole-block self hand-over of the intermediate (eb_ttm2_chain), else
   // nullptr; run_chain launches both for one rank.
   const TermPlan* chain_next(const TermPlan& a) const;
+  static bool fold_shape(const eb_ttm2_desc& da, const eb_ttm2_desc& db);
   void run_chain(const TermPlan& a, const TermPlan& b, std::int64_t rank,
                  const std::map<std::string, const DevBlock*>& at_hand, DevBlock& t1,
                  DevBlock& out);

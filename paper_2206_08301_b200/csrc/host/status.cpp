@@ -46,6 +46,7 @@ Options read_env() {
   if (const char* v = std::getenv("EB_GEMM")) o.gemm = std::atoi(v);
   if (const char* v = std::getenv("EB_FUSE_REDIST")) o.fuse_redistribution = v[0] != '0';
   if (const char* v = std::getenv("EB_CHAIN_TERMS")) o.chain_terms = v[0] != '0';
+  if (const char* v = std::getenv("EB_FOLD_TERMS")) o.fold_terms = v[0] != '0';
   if (const char* v = std::getenv("EB_CHAIN_FLAGS")) o.chain_flags = std::atoi(v);
   if (const char* v = std::getenv("EB_CHAIN_LAG")) o.chain_lag = std::atoi(v);
   if (const char* v = std::getenv("EB_PDL")) o.pdl = v[0] != '0';
@@ -126,6 +127,8 @@ extern "C" int eb_set_option(const char* name, const char* value) {
       o.pdl = v != 0;
     } else if (!std::strcmp(name, "chain_terms")) {
       o.chain_terms = v != 0;
+    } else if (!std::strcmp(name, "fold_terms")) {
+      o.fold_terms = v != 0;
     } else if (!std::strcmp(name, "fuse_redistribution")) {
       o.fuse_redistribution = v != 0;
     } else if (!std::strcmp(name, "gemm")) {

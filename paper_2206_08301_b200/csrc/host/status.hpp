@@ -78,6 +78,12 @@ struct Options {
   // default: measured 1.73 vs 1.60 ms on C5 although t1 never
   // reaches HBM (DRAM writes 534 MB -> 20 MB)
   int chain_terms = 0;
+  // executor: TTMc-O5 terms joined by a self hand-over run as eb_ttmc_fold —
+  // term B's m contraction folded into term A's epilogue, t1 never stored
+  // (ttmc_fold.cu).  Off by default: measured 1.657 vs 1.589 ms on C5 (the
+  // folded contraction's 2.15 GFLOP lands on the DMMA-saturated term-A
+  // kernel).  chain_terms takes precedence when both are on.
+  int fold_terms = 0;
   int chain_flags = 7;    // eb_ttm2_chain cache policy bits (ttm2.cu ChainParams::flags)
   int chain_lag = 1;      // eb_ttm2_chain: term B of slab p runs in group p + lag
   int pdl = 1;            // programmatic dependent launch for the chained kernels

@@ -49,7 +49,7 @@ def ora():
 
 
 _OPTION_DEFAULTS = {"no_fused_tma": 0, "no_rf": 0, "rf_cfg": "auto", "ttm2_variant": 0,
-                    "fuse_ttm2": 1, "gemm": 0, "fuse_redistribution": 1, "chain_terms": 0, "zero_push": 0,
+                    "fuse_ttm2": 1, "gemm": 0, "fuse_redistribution": 1, "chain_terms": 0, "fold_terms": 0, "zero_push": 0,
                     "scatter_fast": 1, "pdl": 1}
 
 

@@ -81,11 +81,11 @@ def test_path_options_set_and_validated_without_gpu(eb):
     from paper_2206_08301_b200 import EinplanError
     for name, good in (("no_fused_tma", 1), ("no_rf", 1), ("rf_cfg", "64x1"),
                        ("ttm2_variant", 2), ("fuse_ttm2", 0), ("gemm", 1),
-                       ("fuse_redistribution", 0), ("chain_terms", 1)):
+                       ("fuse_redistribution", 0), ("chain_terms", 1), ("fold_terms", 1)):
         eb.set_option(name, good)
     for name, value in (("no_fused_tma", 0), ("no_rf", 0), ("rf_cfg", "auto"),
                         ("ttm2_variant", 0), ("fuse_ttm2", 1), ("gemm", 0),
-                        ("fuse_redistribution", 1), ("chain_terms", 0)):
+                        ("fuse_redistribution", 1), ("chain_terms", 0), ("fold_terms", 0)):
         eb.set_option(name, value)
     for name, bad in (("no_such_option", 1), ("ttm2_variant", 7), ("gemm", 3),
                       ("rf_cfg", "sixteen")):

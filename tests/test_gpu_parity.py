@@ -1019,3 +1019,103 @@ def test_back_to_back_runs_are_bitwise_stable(eb, e, ext, P, variant, opts):
         for _ in range(5):
             ex.run()
         assert np.array_equal(ex.gather(), ref)
+
+
+# ---------------------------------------------------- TTMc-O5 fold (m in A) --
+
+def _fold_descs(C, ext, X, U1, U2, U3, U4, out):
+    i, j, k, l, m = (ext[c] for c in "ijklm")
+    b, c, d, e = (ext[s] for s in "bcde")
+    da = C.Ttm2Desc(i, j, k, l * m, b, c, X.data_ptr(), U1.data_ptr(), b, U2.data_ptr(), c, None)
+    db = C.Ttm2Desc(i, l, m, b * c, d, e, None, U3.data_ptr(), d, U4.data_ptr(), e,
+                    out.data_ptr())
+    return da, db
+
+
+@pytest.mark.parametrize("ext", [
+    dict(i=3, j=16, k=16, l=4, m=16, b=16, c=16, d=16, e=16),
+    dict(i=2, j=20, k=13, l=3, m=32, b=12, c=11, d=9, e=13),     # ragged j, k, odd c
+    dict(i=5, j=64, k=64, l=2, m=64, b=16, c=16, d=16, e=16),    # C5 tile shape, l small
+    dict(i=1, j=7, k=5, l=9, m=48, b=5, c=16, d=16, e=1),
+    dict(i=300, j=8, k=4, l=2, m=16, b=4, c=4, d=3, e=2),        # more fold groups than SMs
+])
+def test_ttmc_fold_kernel(eb, ext):
+    """eb_ttmc_fold = both TTMc-O5 terms with term B's m contraction folded
+    into term A's epilogue (t1 never stored), against the oracle's step-by-step
+    reference chain (ijklm -> iklmb -> ilmbc -> imbcd -> ibcde), ragged in
+    every extent the kernel allows; the result must not depend on workspace
+    contents (filled with NaN first)."""
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    e = "ijklm,jb,kc,ld,me->ibcde"
+    ops = oracle.seeded_inputs(e, ext, 97)
+    want = _ttmc_o5_chain(ext, ops)
+    X, U1, U2, U3, U4 = [torch.from_numpy(o).cuda() for o in ops]
+    out = torch.full(want.shape, float("nan"), dtype=torch.float64, device="cuda")
+    da, db = _fold_descs(C, ext, X, U1, U2, U3, U4, out)
+    L = C.lib()
+    wb = L.eb_ttmc_fold_workspace(ctypes.byref(da), ctypes.byref(db))
+    assert wb == 8 * ext["i"] * ext["l"] * ext["e"] * ext["b"] * ext["c"]
+    ws = torch.full((wb // 8,), float("nan"), dtype=torch.float64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for _ in range(2):
+        C.check(L.eb_ttmc_fold(ctypes.byref(da), ctypes.byref(db), ctypes.c_void_p(ws.data_ptr()),
+                               wb, st))
+        torch.cuda.synchronize()
+        check(out.cpu().numpy(), want)
+
+
+def test_ttmc_fold_rejects_unsupported_shapes(eb):
+    from paper_2206_08301_b200 import _capi as C
+    torch = _torch()
+    L = C.lib()
+    buf = torch.zeros(1 << 16, dtype=torch.float64, device="cuda")
+    p = buf.data_ptr()
+    for m, e, d in ((14, 4, 4), (80, 4, 4), (16, 17, 4), (16, 4, 17)):
+        da = C.Ttm2Desc(1, 4, 4, 2 * m, 4, 4, p, p, 4, p, 4, None)
+        db = C.Ttm2Desc(1, 2, m, 16, d, e, None, p, d, p, e, p)
+        assert L.eb_ttmc_fold(ctypes.byref(da), ctypes.byref(db), ctypes.c_void_p(p),
+                              buf.numel() * 8, None) == 1  # EB_E_INVALID
+    da = C.Ttm2Desc(1, 4, 4, 32, 4, 4, p, p, 4, p, 4, None)
+    db = C.Ttm2Desc(1, 2, 16, 16, 4, 4, None, p, 4, p, 4, p)
+    assert L.eb_ttmc_fold(ctypes.byref(da), ctypes.byref(db), ctypes.c_void_p(p), 8, None) == 1
+
+
+@pytest.mark.parametrize("P,ext", [
+    (1, dict(i=16, j=32, k=32, l=32, m=32, b=16, c=16, d=16, e=16)),
+    (2, dict(i=16, j=16, k=16, l=16, m=16, b=12, c=12, d=12, e=12)),
+])
+def test_executor_folds_ttmc_o5_terms(eb, P, ext, opts):
+    """Executor with fold_terms: where the t1 hand-over is a whole-block self
+    message on every rank, the TTMc-O5 terms run as eb_ttmc_fold (2 launches
+    per rank, t1 not stored); same output as the two-launch path (fold_terms 0)
+    and the oracle chain, repeatedly."""
+    e = "ijklm,jb,kc,ld,me->ibcde"
+    plan_r = json.loads(eb.plan_json(e, ext, P, include_messages=True))
+    assert [t["output"] for t in plan_r["schedule"]["terms"]] == ["t1", "out"]
+    assert all(m["self"] for r in plan_r["schedule"]["redistributions"]
+               for m in r["plan"]["messages"])
+    ops = oracle.seeded_inputs(e, ext, 13)
+    want = _ttmc_o5_chain(ext, ops)
+    opts("fold_terms", 0)
+    ref = eb.Executor(e, ext, P)
+    ref.stage(ops)
+    ref.run()
+    two = ref.gather().copy()
+    st0 = ref.stats()
+    ref.close()
+    check(two, want)
+    opts("fold_terms", 1)
+    ex = eb.Executor(e, ext, P)
+    ex.stage(ops)
+    n0 = eb.launch_count()
+    ex.run()
+    st = ex.stats()
+    assert st["fused_launches"] == 2 * P and st["generic_launches"] == 0, st
+    assert st["redistribute_volume"] == st0["redistribute_volume"]
+    assert eb.launch_count() - n0 >= 2 * P
+    for _ in range(3):
+        ex.run()
+        got = ex.gather()
+        check(got, want)
+        check(got, two)
