@@ -514,6 +514,7 @@ def main():
     ranked = use_nccl or peer
     stream = torch.cuda.Stream()
     execs, inputs, grids, flops_tree = [], [], [], 0
+    q_bound_total = 0.0  # SOAP I/O lower bound of every mode's partition (soap.cpp:359-425)
     x_shared = []  # per executor: is operand 0 (X) aliased to executor 0's blocks?
     # one process per GPU: stage only this rank's boxes (EB_BENCH_BLOCKS=1
     # forces it for a single NCCL rank, to exercise the path on one GPU)
@@ -545,6 +546,7 @@ def main():
         x_shared.append(shared)
         plan = json.loads(eb.plan_json(e, ext, P))
         grids.append([t["grid"] for t in plan["schedule"]["terms"]])
+        q_bound_total += float(plan["partition"]["total_q"])
         flops_tree += plan["tree"]["total_flops"]
     torch.cuda.synchronize()
 
@@ -599,6 +601,7 @@ def main():
     clocks.start()
     ms, launches, _, _ = timed(False)
     ms_kpass, _, kms, kn = timed(True)  # the same K steps again: the roofline's kernel time
+    comm = _communication(execs, q_bound_total)  # before the dimension-tree / CP-ALS extras
     clk = clocks.stop()
     if world > 1:
         ms = _max_over_ranks(ms)
@@ -745,6 +748,7 @@ def main():
                    "l2": "inputs larger than L2 (X is %.2f GB per GPU vs 126 MB L2), no flush "
                          "needed" % (_x_bytes(modes[:1], P) / 1e9)},
         "roofline": roof,
+        "communication": comm,
         "e2e": e2e,
         **({"sweep_dimtree": alt} if alt else {}),
         **({"cp_als": als} if als else {}),
@@ -760,6 +764,27 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _communication(execs, q_bound_total):
+    """Reduction / exchange volume of one step against the derived I/O lower
+    bound, with the reference's accounting (CommStats, executor.cpp:103-105,
+    193-198; einplan_bench_json's volume_to_bound_ratio, bench.cpp:79-87):
+    allreduce = block elements x (group - 1), redistribute = transmitted
+    volume of the non-self messages, bound = the chosen partition's total_q
+    (SOAP, S = 1024), summed over the step's einsums."""
+    ar = rd = mx = 0
+    for ex in execs:
+        st = ex.stats()
+        ar += int(st["allreduce_volume"])
+        rd += int(st["redistribute_volume"])
+        mx += int(st["max_rank_sent"])
+    tot = ar + rd
+    return {"allreduce_elems": ar, "redistribute_elems": rd, "volume_total_elems": tot,
+            "volume_total_bytes": 8 * tot, "max_rank_sent_bytes": 8 * mx,
+            "q_bound_total_elems": q_bound_total,
+            "volume_to_bound_ratio": (tot / q_bound_total) if q_bound_total > 0 else None,
+            "accounting": "reference CommStats / bench.cpp:79-87 (elements; bytes = 8x)"}
 
 
 def _other_configs(args):
@@ -780,7 +805,8 @@ def _other_configs(args):
                       "ms_per_step": l["ms_per_step"], "bound": ro["bound"],
                       "achieved": ro["achieved"], "peak": ro["peak"], "roof_unit": ro["unit"],
                       "frac": ro["frac"], "kernel": ro.get("kernel"),
-                      "gpu_launches": l.get("gpu_launches"), "clocks": l.get("clocks")}
+                      "gpu_launches": l.get("gpu_launches"), "clocks": l.get("clocks"),
+                      "communication": l.get("communication")}
         except Exception as e:  # reported, never fatal for the headline
             out[c] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out
