@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 FP64_PEAK_TFLOPS = 37.05   # measured DMMA.8x8x4 peak on this pool's B200 (profiles/fp64_peak_r01.jsonl)
+FP64_PEAK_CLOCK_MHZ = 1965  # the SM clock that peak was measured at (same file, first line)
 HBM_READ_GBS = 7182.5      # measured read-only stream (same file)
 
 
@@ -702,6 +703,14 @@ def main():
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
             "algorithmic_flops_per_launch": per_launch_flops,
             "launches_per_step": launches_per_step}
+    # The FP64 peak was measured at 1965 MHz (profiles/fp64_peak_r01.jsonl); DMMA
+    # throughput scales with the SM clock, so under a power cap the attainable
+    # peak is lower: reported beside the fixed denominator, not instead of it.
+    run_mhz = (clk or {}).get("sm_mhz") if isinstance(clk, dict) else None
+    if run_mhz:
+        roof["peak_clock_mhz"] = FP64_PEAK_CLOCK_MHZ
+        roof["fp64_peak_at_run_clock"] = FP64_PEAK_TFLOPS * run_mhz / FP64_PEAK_CLOCK_MHZ
+        roof["fp64_frac_at_run_clock"] = achieved / roof["fp64_peak_at_run_clock"]
     if args.config == "C5":
         # C5 sits at the HBM side of the ridge (1.316 ms of HBM vs
         # 1.233 ms of FP64 per GPU): the binding roof is bandwidth.  Algorithmic
