@@ -379,6 +379,11 @@ void run_fold(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* ws, size_t wsb
               cudaStream_t st) {
   validate_fold(a, b);
   if (!ws || wsb < fold_workspace(a, b)) throw InvalidError("eb_ttmc_fold: workspace too small");
+  // the tail kernel's limits, checked before anything is launched
+  if ((b->Q1 * kNB + kTailS * kTailPitch) * 8 > 227 * 1024)
+    throw InvalidError("eb_ttmc_fold: Q1b too large for the tail kernel");
+  if (b->P * ((b->M + kTailS - 1) / kTailS) >= (int64_t(1) << 31))
+    throw InvalidError("eb_ttmc_fold: too many (q, 16-column) tail blocks for one launch");
   check_device();
   FoldParams prm;
   std::memset(&prm, 0, sizeof(prm));
@@ -427,7 +432,6 @@ void run_fold(const eb_ttm2_desc* a, const eb_ttm2_desc* b, void* ws, size_t wsb
   tp.ldu3 = b->ldu1;
   tp.out = b->out;
   const int tsmem = (int)((tp.L * kNB + kTailS * kTailPitch) * 8);
-  if (tsmem > 227 * 1024) throw InvalidError("eb_ttmc_fold: Q1b too large for the tail kernel");
   set_smem_once(ttmc_tail_kernel, 227 * 1024);  // once per device: the largest L any call may use
   main_kernel_begin(st);
   launch_pdl(ttmc_tail_kernel, dim3((unsigned)(tp.Q * tp.schunks)), dim3(256), tsmem, st, tp);
