@@ -27,3 +27,30 @@ def test_communication_sums_modes_against_the_bound():
 def test_communication_without_a_bound():
     c = bench._communication([_Ex(0, 0, 0)], 0.0)
     assert c["volume_total_elems"] == 0 and c["volume_to_bound_ratio"] is None
+
+
+def _bench(args, env_extra=None):
+    import subprocess
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env.update(env_extra or {})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args],
+                          capture_output=True, text=True, timeout=300, env=env)
+
+
+def test_gpus_n_refuses_a_box_with_fewer_gpus():
+    """`bench.py --gpus 2` never prints an n_gpus=1 line: on a box with fewer
+    GPUs (none here) it exits 2 with the reason on stderr."""
+    r = _bench(["--gpus", "2", "--steps", "1", "--warmup", "1"])
+    assert r.returncode == 2, (r.returncode, r.stderr[-500:])
+    assert "needs 2 GPUs" in r.stderr
+    assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_gpus_must_match_world_size():
+    """Launched under torchrun, --gpus and WORLD_SIZE must agree."""
+    r = _bench(["--gpus", "2", "--steps", "1", "--warmup", "1"],
+               {"WORLD_SIZE": "4", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2, (r.returncode, r.stderr[-500:])
+    assert "WORLD_SIZE=4" in r.stderr
